@@ -1,0 +1,118 @@
+/* slsht_cuda.h — C ABI of the B200-native directional-SLSHT forward engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   slsht::forward_fast(f, h, sink, opts)   /root/reference/proj/include/slsht/transform.hpp:162-163
+ *   slsht::forward_fast(f, h, opts)         /root/reference/proj/include/slsht/transform.hpp:164-165
+ * (implemented at /root/reference/proj/src/transform.cpp:244-311). The reference has no FFI;
+ * its callers are C++ (proj/src/cli.cpp:223-224, proj/tests/acceptance_main.cpp:97). The C++
+ * shim paper_1207_5558_b200/csrc/forward_fast_shim.cpp implements both forward_fast overloads
+ * against the UNCHANGED reference headers on top of this ABI; Python tests and bench.py bind it
+ * with ctypes (paper_1207_5558_b200/_lib.py). See INTEGRATION.md.
+ *
+ * Conventions (all from the reference):
+ *  - complex arrays are interleaved (re, im) doubles == std::complex<double> storage;
+ *  - coefficient arrays (f, h) are indexed coeff_index(l, m) = l*l + l + m
+ *    (proj/include/slsht/harmonics.hpp:13), (L+1)^2 entries;
+ *  - a component volume is an So3Volume: n*(L_h+1)*n complex, index (a*(L_h+1)+b)*n + c,
+ *    n = 2*L_h+1 (proj/include/slsht/transform.hpp:15-29);
+ *  - status codes: 0 ok, 2 validation (slsht::ValidationError, CLI exit 2), 3 numeric
+ *    (slsht::NumericError, CLI exit 3), 4 device/runtime (CUDA), matching
+ *    proj/include/slsht/errors.hpp and proj/src/cli.cpp:31-45.
+ *
+ * There is no CPU fallback: every entry point that computes runs CUDA kernels built for sm_100a
+ * and returns SLSHT_ERR_DEVICE when no suitable device is present.
+ */
+#ifndef SLSHT_CUDA_H
+#define SLSHT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLSHT_OK 0
+#define SLSHT_ERR_VALIDATION 2
+#define SLSHT_ERR_NUMERIC 3
+#define SLSHT_ERR_DEVICE 4
+
+/* Per-component digest computed on the device by the fused epilogue (8 doubles):
+ *  [0] sum |g_i|^2          [1] max |g_i|
+ *  [2,3] sum w_i g_i         with w_i = ((uint32(i) * 0x9E3779B1u) >> 8) * 2^-24 - 0.5
+ *  [4,5] g at (a, b, c) = (0, 0, 0)
+ *  [6,7] integrate_volume(g) = (2L_h+1)^-3 sum_{a,b,c} q(beta_b) g  (proj/src/transform.cpp:469-485)
+ * Dividing [6,7] by sqrt(16 pi^3) h_0^0 gives the inverse coefficient f_l^m for l <= L_f
+ * (InverseAccumulator, proj/src/transform.cpp:502-540). */
+#define SLSHT_DIGEST_WIDTH 8
+
+typedef struct slsht_cuda_plan slsht_cuda_plan;
+
+typedef struct slsht_cuda_desc {
+  int L_f;             /* f.band_limit */
+  int L_h;             /* h.band_limit */
+  int lmax;            /* ForwardOptions::lmax; -1 means L_f + L_h (transform.hpp:146-148) */
+  int real_mode;       /* use_real_symmetry && f.real_signal && h.real_signal (transform.cpp:253-254) */
+  int emit_negative_m; /* ForwardOptions::emit_negative_m (transform.hpp:154-156) */
+  int device;          /* CUDA device ordinal */
+  int l_begin;         /* first degree computed by this plan (multi-GPU shard); 0 for all */
+  int l_end;           /* one past the last degree; -1 means lmax + 1 */
+  int materialize;     /* 1: keep every emitted volume resident on the device at slot
+                          coeff_index(l, m) (the materialized forward_fast, transform.cpp:297-311);
+                          0: stream volumes through a device ring consumed by the epilogue */
+  int reserved0;
+  long long ring_bytes; /* ring capacity for materialize == 0 (0: automatic) */
+  void* stream;        /* cudaStream_t to run on (NULL: the plan creates its own) */
+} slsht_cuda_desc;
+
+/* Host sink, called once per emitted component with a pointer valid only during the call
+ * (the So3Volume& contract of ComponentSink, transform.hpp:142-143, transform.cpp:279-284).
+ * Calls are serialized on the calling thread. */
+typedef void (*slsht_host_sink)(int l, int m, const double* volume, void* user);
+
+int slsht_cuda_plan_create(const slsht_cuda_desc* desc, slsht_cuda_plan** plan);
+void slsht_cuda_plan_destroy(slsht_cuda_plan* plan);
+/* Message of the last failure on this plan (or of the last failed plan_create when plan is NULL). */
+const char* slsht_cuda_last_error(const slsht_cuda_plan* plan);
+
+/* forward_fast(f, h, sink, opts): f, h host arrays; every emitted component of the plan's
+ * degree range is delivered to the sink (pinned, double-buffered D2H). */
+int slsht_cuda_forward(slsht_cuda_plan* plan, const double* f, const double* h,
+                       slsht_host_sink sink, void* user);
+
+/* Device-consumer mode (the timed mode of bench.py). f, h are host pointers unless
+ * inputs_on_device != 0. digests (may be NULL) receives coeff_count(lmax) x 8 doubles at
+ * coeff_index(l, m) for every emitted component of the plan's shard (other rows untouched);
+ * it is a host pointer unless digests_on_device != 0. With synchronize == 0 the call only
+ * enqueues work on the plan's stream (digests must then be a device pointer). */
+int slsht_cuda_forward_device(slsht_cuda_plan* plan, const double* f, const double* h,
+                              int inputs_on_device, double* digests, int digests_on_device,
+                              int synchronize);
+
+/* Device pointer to the materialized distribution (materialize == 1): coeff_count(lmax)
+ * volumes, volume k at offset k * volume_elems complex. NULL in ring mode. */
+const double* slsht_cuda_device_output(const slsht_cuda_plan* plan);
+long long slsht_cuda_volume_elems(const slsht_cuda_plan* plan);
+long long slsht_cuda_computed_count(const slsht_cuda_plan* plan);
+long long slsht_cuda_emitted_count(const slsht_cuda_plan* plan);
+void* slsht_cuda_stream(const slsht_cuda_plan* plan);
+
+/* Kernel launches issued by the last forward call, and per-stage device time (ms, CUDA
+ * events on the plan stream) when SLSHT_CUDA_PROFILE=1 was set at plan creation:
+ * out[0] setup tables, [1] Legendre rows, [2] modulated-SHT GEMM, [3] coupling + alpha FFT
+ * + epilogue, [4] digest reduction. Returns the number of entries written. */
+long long slsht_cuda_launch_count(const slsht_cuda_plan* plan);
+int slsht_cuda_stage_times(const slsht_cuda_plan* plan, double* out_ms, int n);
+
+/* Component-level entry points (host arrays in/out), mirroring the reference's
+ * DeltaTables (wigner.cpp:28-80), ModulatedSht::compute (transform.cpp:189-220) and the
+ * window-side table of the coupling stage; used by the parity tests. */
+int slsht_cuda_delta_tables(int device, int L, double* out);
+/* mod for (l[i], m[i]), i < count: out is count x coeff_count(L_h) complex, coeff_index(p, q). */
+int slsht_cuda_modulated(slsht_cuda_plan* plan, const double* f, int count, const int* l,
+                         const int* m, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLSHT_CUDA_H */

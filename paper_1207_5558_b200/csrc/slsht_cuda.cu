@@ -1,0 +1,779 @@
+// Host side of the B200 directional-SLSHT engine: plan construction, chunk scheduling and the
+// extern "C" ABI declared in include/slsht_cuda.h. All arithmetic runs in the kernels of
+// kernels.cuh; the host only builds index tables (component lists, FFT plan, q offsets).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "slsht_cuda.h"
+
+using namespace slsht_cuda;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct CudaError {
+  std::string msg;
+};
+struct Status {
+  int code;
+  std::string msg;
+};
+
+#define CK(x)                                                                         \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      throw CudaError{std::string(#x) + ": " + cudaGetErrorString(e_)};               \
+  } while (0)
+
+#define CKL()                                                                         \
+  do {                                                                                \
+    cudaError_t e_ = cudaGetLastError();                                              \
+    if (e_ != cudaSuccess) throw CudaError{std::string("launch: ") + cudaGetErrorString(e_)}; \
+  } while (0)
+
+inline int coeff_index(int l, int m) { return l * l + l + m; }
+inline long long coeff_count(int L) { return (long long)(L + 1) * (L + 1); }
+
+template <class T>
+T* dalloc(size_t count) {
+  T* p = nullptr;
+  if (count == 0) count = 1;
+  CK(cudaMalloc(&p, count * sizeof(T)));
+  return p;
+}
+
+template <class T>
+T* dupload(const std::vector<T>& v, cudaStream_t s) {
+  T* p = dalloc<T>(v.size());
+  if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return p;
+}
+
+struct Chunk {
+  long long comp0;
+  int count;
+  int seg0, nseg;
+  int tile0, ntile;
+  int buf;  // ring half (ring mode)
+};
+
+enum Stage { ST_SETUP = 0, ST_LEGENDRE, ST_MODGEMM, ST_COUPLE, ST_DIGEST, ST_COUNT };
+
+}  // namespace
+
+struct slsht_cuda_plan {
+  slsht_cuda_desc desc{};
+  int L_f = 0, L_h = 0, L_g = 0, lmax = 0, l_begin = 0, l_end = 0;
+  int n = 0, nb = 0, ncol = 0, NPQ = 0, N = 0, n_nodes = 0, ldA = 0;
+  int real_mode = 0, emit_neg = 0, mirror = 0, materialize = 0;
+  int MG = 1, NG = 1, n_col_tiles = 0;
+  long long vol = 0;            // complex elements per volume
+  long long slot_base = 0;      // coeff_index offset of the first materialized slot
+  long long n_slots = 0;        // output slots allocated
+  long long emitted = 0;
+  int max_chunk = 0;
+  FftPlan fft{};
+  int generic_dft = 0;
+  size_t couple_smem = 0;
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  bool own_stream = false;
+  bool profile = false;
+  std::string last_error;
+  long long launches = 0;
+  double stage_ms[ST_COUNT] = {0, 0, 0, 0, 0};
+
+  std::vector<CompRec> comps;
+  std::vector<Seg> segs;
+  std::vector<MTile> tiles;
+  std::vector<Chunk> chunks;
+
+  // device
+  double *d_f = nullptr, *d_h = nullptr;
+  double *d_ncos = nullptr, *d_nsin = nullptr, *d_weights = nullptr, *d_betaw = nullptr;
+  double2* d_itab = nullptr;
+  double* d_lamh = nullptr;
+  double* d_delta = nullptr;
+  double* d_dtab = nullptr;
+  double2* d_W = nullptr;
+  double2* d_rou = nullptr;
+  double2* d_phase = nullptr;
+  int* d_perm = nullptr;
+  int* d_qoff = nullptr;
+  int* d_pq = nullptr;
+  int* d_err = nullptr;
+  CompRec* d_comps = nullptr;
+  Seg* d_segs = nullptr;
+  MTile* d_tiles = nullptr;
+  double* d_A = nullptr;
+  double2* d_U = nullptr;
+  double2* d_out = nullptr;
+  double* d_partials = nullptr;
+  double* d_digest = nullptr;
+  long long digest_rows = 0;
+  // host staging for the host-sink mode
+  double2* h_stage[2] = {nullptr, nullptr};
+  size_t stage_bytes = 0;
+  cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
+  cudaEvent_t ev_stage[ST_COUNT + 1] = {};
+};
+
+namespace {
+
+void free_plan(slsht_cuda_plan* p) {
+  if (!p) return;
+  cudaFree(p->d_f);
+  cudaFree(p->d_h);
+  cudaFree(p->d_ncos);
+  cudaFree(p->d_nsin);
+  cudaFree(p->d_weights);
+  cudaFree(p->d_betaw);
+  cudaFree(p->d_itab);
+  cudaFree(p->d_lamh);
+  cudaFree(p->d_delta);
+  cudaFree(p->d_dtab);
+  cudaFree(p->d_W);
+  cudaFree(p->d_rou);
+  cudaFree(p->d_phase);
+  cudaFree(p->d_perm);
+  cudaFree(p->d_qoff);
+  cudaFree(p->d_pq);
+  cudaFree(p->d_err);
+  cudaFree(p->d_comps);
+  cudaFree(p->d_segs);
+  cudaFree(p->d_tiles);
+  cudaFree(p->d_A);
+  cudaFree(p->d_U);
+  cudaFree(p->d_out);
+  cudaFree(p->d_partials);
+  cudaFree(p->d_digest);
+  for (int i = 0; i < 2; ++i) {
+    if (p->h_stage[i]) cudaFreeHost(p->h_stage[i]);
+    if (p->ev_done[i]) cudaEventDestroy(p->ev_done[i]);
+    if (p->ev_copied[i]) cudaEventDestroy(p->ev_copied[i]);
+  }
+  for (auto& e : p->ev_stage)
+    if (e) cudaEventDestroy(e);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+}
+
+std::vector<int> factor_odd(int n) {
+  std::vector<int> f;
+  int x = n;
+  for (int p = 3; x > 1; p += 2)
+    while (x % p == 0) {
+      f.push_back(p);
+      x /= p;
+    }
+  return f;
+}
+
+// Tile shape of k_couple per transform length: the CTA keeps 8*MG x 8*NG x n complex of T in
+// shared memory (<= ~135 KB), DESIGN.md §3.3.
+void couple_tile(int n, int& MG, int& NG) {
+  if (n <= 33) {
+    MG = 2;
+    NG = 2;
+  } else if (n <= 65) {
+    MG = 2;
+    NG = 1;
+  } else {
+    MG = 1;
+    NG = 1;
+  }
+}
+
+size_t couple_smem_bytes(int n, int MG, int NG) {
+  const size_t T = std::max<size_t>((size_t)64 * MG * NG * n * 16, 256 * 8 * 8);
+  return T + (size_t)n * 16 * 2 + (size_t)((n + 1) & ~1) * 4 + (size_t)(n / 2 + 1) * 8 + 64;
+}
+
+template <int MG, int NG>
+void set_couple_attr(size_t smem) {
+  CK(cudaFuncSetAttribute(k_couple<MG, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+}
+
+template <int MG, int NG>
+void launch_couple_t(const CoupleParams& prm, dim3 grid, size_t smem, cudaStream_t s) {
+  k_couple<MG, NG><<<grid, 256, smem, s>>>(prm);
+}
+
+void launch_couple(int MG, int NG, const CoupleParams& prm, dim3 grid, size_t smem,
+                   cudaStream_t s) {
+  if (MG == 2 && NG == 2) launch_couple_t<2, 2>(prm, grid, smem, s);
+  else if (MG == 2 && NG == 1) launch_couple_t<2, 1>(prm, grid, smem, s);
+  else launch_couple_t<1, 1>(prm, grid, smem, s);
+}
+
+void build_plan(slsht_cuda_plan* p) {
+  const slsht_cuda_desc& d = p->desc;
+  if (d.L_f < 0 || d.L_h < 0) throw Status{SLSHT_ERR_VALIDATION, "band limit must be non-negative"};
+  p->L_f = d.L_f;
+  p->L_h = d.L_h;
+  p->L_g = d.L_f + d.L_h;
+  p->lmax = d.lmax < 0 ? p->L_g : d.lmax;
+  if (p->lmax > p->L_g)
+    throw Status{SLSHT_ERR_VALIDATION, "fast engine computes components up to L_f + L_h only"};
+  if (2 * d.L_h + 1 > 221)
+    throw Status{SLSHT_ERR_VALIDATION, "window band limit above 110 is not supported by this build"};
+  p->l_begin = std::max(0, d.l_begin);
+  p->l_end = d.l_end < 0 ? p->lmax + 1 : std::min(d.l_end, p->lmax + 1);
+  if (p->l_begin > p->l_end) throw Status{SLSHT_ERR_VALIDATION, "empty or inverted degree range"};
+  p->real_mode = d.real_mode ? 1 : 0;
+  p->emit_neg = d.emit_negative_m ? 1 : 0;
+  p->mirror = p->real_mode && p->emit_neg;
+  p->materialize = d.materialize ? 1 : 0;
+  const int L = p->L_h;
+  p->n = 2 * L + 1;
+  p->nb = L + 1;
+  p->ncol = p->n * p->nb;
+  p->NPQ = (L + 1) * (L + 1);
+  p->N = 2 * p->L_g;
+  p->n_nodes = p->N + 1;
+  p->ldA = (p->n_nodes + MG_K - 1) / MG_K * MG_K;
+  p->vol = (long long)p->n * p->n * p->nb;
+  couple_tile(p->n, p->MG, p->NG);
+  p->n_col_tiles = (p->ncol + 8 * p->NG - 1) / (8 * p->NG);
+  const char* prof = std::getenv("SLSHT_CUDA_PROFILE");
+  p->profile = prof && prof[0] == '1';
+
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+    throw Status{SLSHT_ERR_DEVICE, "no CUDA device available (the engine has no CPU fallback)"};
+  if (d.device < 0 || d.device >= dev_count) throw Status{SLSHT_ERR_DEVICE, "invalid device ordinal"};
+  CK(cudaSetDevice(d.device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, d.device));
+  if (prop.major != 10) throw Status{SLSHT_ERR_DEVICE, "this build targets sm_100a (B200) only"};
+
+  if (d.stream) {
+    p->stream = (cudaStream_t)d.stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    p->own_stream = true;
+  }
+  CK(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+  cudaStream_t s = p->stream;
+
+  // ---- q-major (p, q) ordering of the window band: c = qoff[q+L] + p - |q|
+  std::vector<int> qoff(p->n + 1, 0), pq(2 * p->NPQ);
+  for (int jq = 0; jq < p->n; ++jq) {
+    const int q = jq - L, aq = std::abs(q);
+    qoff[jq + 1] = qoff[jq] + (L + 1 - aq);
+    for (int pp = aq; pp <= L; ++pp) {
+      const int c = qoff[jq] + pp - aq;
+      pq[2 * c] = q;
+      pq[2 * c + 1] = pp;
+    }
+  }
+  // ---- alpha-axis FFT plan: roots of unity, DIF stages, output permutation, phase shift
+  const int n = p->n;
+  std::vector<double2> rou(n), phase(n);
+  for (int k = 0; k < n; ++k) {
+    const double ang = -2.0 * kPi * k / n;
+    rou[k] = make_double2(std::cos(ang), std::sin(ang));
+  }
+  for (int a = 0; a < n; ++a) {
+    const int e = (int)(((long long)L * a) % n);  // e^{+2 pi i L a / n} = conj(rou[e])
+    phase[a] = make_double2(rou[e].x, -rou[e].y);
+  }
+  const std::vector<int> fac = factor_odd(n);
+  p->generic_dft = 0;
+  for (int r : fac)
+    if (r > kMaxGeneratedRadix) p->generic_dft = 1;
+  if (fac.size() > 8) p->generic_dft = 1;
+  std::vector<int> perm(n, 0);
+  if (!p->generic_dft) {
+    p->fft.nstages = (int)fac.size();
+    int m = n;
+    for (size_t i = 0; i < fac.size(); ++i) {
+      p->fft.radix[i] = fac[i];
+      p->fft.span[i] = m;
+      m /= fac[i];
+    }
+    for (int pos = 0; pos < n; ++pos) {
+      int rem = pos, freq = 0, mult = 1, mm = n;
+      for (int r : fac) {
+        const int mp = mm / r, k = rem / mp;
+        rem %= mp;
+        freq += k * mult;
+        mult *= r;
+        mm = mp;
+      }
+      perm[freq] = pos;
+    }
+  } else {
+    p->fft.nstages = 0;
+    for (int a = 0; a < n; ++a) perm[a] = a;
+  }
+
+  // ---- component list: orders m (all or m >= 0 in real mode), degrees in the shard
+  for (int m = p->real_mode ? 0 : -p->lmax; m <= p->lmax; ++m) {
+    const int lo = std::max(std::abs(m), p->l_begin), hi = std::min(p->lmax, p->l_end - 1);
+    for (int l = lo; l <= hi; ++l) p->comps.push_back(CompRec{l, m, 0, -1});
+  }
+  const long long total = (long long)p->comps.size();
+  p->emitted = 0;
+  for (const auto& c : p->comps) p->emitted += (p->mirror && c.m > 0) ? 2 : 1;
+
+  // ---- chunking and output slots
+  const size_t vol_bytes = (size_t)p->vol * 16;
+  if (p->materialize) {
+    p->slot_base = (long long)p->l_begin * p->l_begin;
+    p->n_slots = (long long)p->l_end * p->l_end - p->slot_base;
+    p->max_chunk = (int)std::min<long long>(std::max<long long>(total, 1), 16384);
+  } else {
+    long long ring = d.ring_bytes > 0 ? d.ring_bytes : (1LL << 31);
+    const int per = p->mirror ? 2 : 1;
+    long long ch = ring / (2LL * per * (long long)vol_bytes);
+    ch = std::max<long long>(8, ch / 8 * 8);
+    ch = std::min<long long>(ch, 16384);
+    ch = std::min<long long>(ch, std::max<long long>(8, (total + 7) / 8 * 8));
+    p->max_chunk = (int)ch;
+    p->n_slots = 2LL * per * ch;
+  }
+  for (long long c0 = 0, ci = 0; c0 < total; c0 += p->max_chunk, ++ci) {
+    Chunk ch{};
+    ch.comp0 = c0;
+    ch.count = (int)std::min<long long>(p->max_chunk, total - c0);
+    ch.buf = (int)(ci & 1);
+    ch.seg0 = (int)p->segs.size();
+    ch.tile0 = (int)p->tiles.size();
+    int i = 0;
+    while (i < ch.count) {
+      const int m = p->comps[c0 + i].m;
+      int j = i;
+      while (j + 1 < ch.count && p->comps[c0 + j + 1].m == m) ++j;
+      p->segs.push_back(Seg{m, p->comps[c0 + i].l, p->comps[c0 + j].l, i});
+      for (int r = i; r <= j; r += MG_ROWS)
+        p->tiles.push_back(MTile{m, r, std::min(MG_ROWS, j - r + 1)});
+      i = j + 1;
+    }
+    ch.nseg = (int)p->segs.size() - ch.seg0;
+    ch.ntile = (int)p->tiles.size() - ch.tile0;
+    const int per = p->mirror ? 2 : 1;
+    for (int k = 0; k < ch.count; ++k) {
+      CompRec& r = p->comps[c0 + k];
+      if (p->materialize) {
+        r.slot = coeff_index(r.l, r.m) - p->slot_base;
+        r.mslot = (p->mirror && r.m > 0) ? coeff_index(r.l, -r.m) - p->slot_base : -1;
+      } else {
+        const long long half = (long long)ch.buf * per * p->max_chunk;
+        r.slot = half + k;
+        r.mslot = (p->mirror && r.m > 0) ? half + p->max_chunk + k : -1;
+      }
+    }
+    p->chunks.push_back(ch);
+  }
+
+  // ---- device memory
+  const int Lf = p->L_f;
+  p->d_f = dalloc<double>(2 * coeff_count(Lf));
+  p->d_h = dalloc<double>(2 * coeff_count(L));
+  CK(cudaMemsetAsync(p->d_h, 0, sizeof(double) * 2 * coeff_count(L), s));
+  CK(cudaMemsetAsync(p->d_f, 0, sizeof(double) * 2 * coeff_count(Lf), s));
+  p->d_ncos = dalloc<double>(p->n_nodes);
+  p->d_nsin = dalloc<double>(p->n_nodes);
+  p->d_weights = dalloc<double>(p->n_nodes);
+  p->d_betaw = dalloc<double>(p->nb);
+  p->d_itab = dalloc<double2>((size_t)(2 * Lf + 1) * p->n_nodes);
+  p->d_lamh = dalloc<double>((size_t)p->NPQ * p->n_nodes);
+  size_t dsz = 0;
+  for (int pp = 0; pp <= L; ++pp) dsz += (size_t)(2 * pp + 1) * (2 * pp + 1);
+  p->d_delta = dalloc<double>(dsz);
+  p->d_dtab = dalloc<double>(dsz * p->nb);
+  p->d_W = dalloc<double2>((size_t)p->NPQ * p->ncol);
+  p->d_rou = dupload(rou, s);
+  p->d_phase = dupload(phase, s);
+  p->d_perm = dupload(perm, s);
+  p->d_qoff = dupload(qoff, s);
+  p->d_pq = dupload(pq, s);
+  p->d_err = dalloc<int>(1);
+  CK(cudaMemsetAsync(p->d_err, 0, sizeof(int), s));
+  p->d_comps = dupload(p->comps, s);
+  p->d_segs = dupload(p->segs, s);
+  p->d_tiles = dupload(p->tiles, s);
+  p->d_A = dalloc<double>((size_t)p->max_chunk * p->ldA);
+  p->d_U = dalloc<double2>((size_t)p->max_chunk * p->NPQ);
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const size_t out_bytes = (size_t)p->n_slots * vol_bytes;
+  if (out_bytes + (64u << 20) > free_b)
+    throw Status{SLSHT_ERR_VALIDATION,
+                 "device output buffer does not fit in HBM (use the streaming ring mode)"};
+  p->d_out = dalloc<double2>((size_t)p->n_slots * p->vol);
+  p->d_partials = dalloc<double>((size_t)p->max_chunk * p->n_col_tiles * 8);
+  p->digest_rows = coeff_count(p->lmax);
+  p->d_digest = dalloc<double>((size_t)p->digest_rows * 8);
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaEventCreateWithFlags(&p->ev_done[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->ev_copied[i], cudaEventDisableTiming));
+  }
+  for (auto& e : p->ev_stage) CK(cudaEventCreate(&e));
+
+  p->couple_smem = couple_smem_bytes(p->n, p->MG, p->NG);
+  if (p->couple_smem > (size_t)prop.sharedMemPerBlockOptin)
+    throw Status{SLSHT_ERR_VALIDATION, "window band limit too large for the shared-memory tile"};
+  if (p->MG == 2 && p->NG == 2) set_couple_attr<2, 2>(p->couple_smem);
+  else if (p->MG == 2 && p->NG == 1) set_couple_attr<2, 1>(p->couple_smem);
+  else set_couple_attr<1, 1>(p->couple_smem);
+  CK(cudaStreamSynchronize(s));
+}
+
+void record(slsht_cuda_plan* p, int idx) {
+  if (p->profile) CK(cudaEventRecord(p->ev_stage[idx], p->stream));
+}
+
+void accumulate(slsht_cuda_plan* p, int st, int a, int b) {
+  if (!p->profile) return;
+  CK(cudaEventSynchronize(p->ev_stage[b]));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, p->ev_stage[a], p->ev_stage[b]));
+  p->stage_ms[st] += ms;
+}
+
+// Setup stage: every table that depends on f, h or the band limits (recomputed per call).
+void run_setup(slsht_cuda_plan* p) {
+  cudaStream_t s = p->stream;
+  const int L = p->L_h;
+  record(p, 0);
+  k_nodes<<<(p->n_nodes + 127) / 128, 128, 0, s>>>(p->N, p->d_ncos, p->d_nsin, p->d_weights, L,
+                                                   p->d_betaw, p->d_err);
+  CKL();
+  k_legendre_window<<<dim3((p->n_nodes + 127) / 128, p->n), 128, 0, s>>>(
+      L, p->n_nodes, p->d_ncos, p->d_nsin, p->d_qoff, p->d_lamh);
+  CKL();
+  k_itab<<<dim3((p->n_nodes + 127) / 128, 2 * p->L_f + 1), 128, 0, s>>>(
+      p->L_f, p->n_nodes, p->d_ncos, p->d_nsin, p->d_f, reinterpret_cast<double*>(p->d_itab));
+  CKL();
+  const size_t dsm = sizeof(double) * ((size_t)(L + 1) * (L + 1) + (L + 1));
+  k_delta<<<1, 128, dsm, s>>>(L, p->d_delta);
+  CKL();
+  const int wmax = (2 * L + 1) * (2 * L + 1) * p->nb;
+  k_dtab<<<dim3((wmax + 255) / 256, L + 1), 256, 0, s>>>(L, p->d_delta, p->d_rou, p->d_dtab);
+  CKL();
+  k_wtab<<<dim3((p->ncol + 127) / 128, p->NPQ), 128, 0, s>>>(L, p->d_h, p->d_dtab, p->d_rou,
+                                                             p->d_pq, p->d_W);
+  CKL();
+  p->launches += 6;
+  record(p, 1);
+  accumulate(p, ST_SETUP, 0, 1);
+}
+
+void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
+  cudaStream_t s = p->stream;
+  const CompRec* comps = p->d_comps + ch.comp0;
+  record(p, 0);
+  k_agen<<<dim3(ch.nseg, (p->ldA + 127) / 128), 128, 0, s>>>(
+      p->d_segs + ch.seg0, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_weights, p->d_A);
+  CKL();
+  record(p, 1);
+  k_modgemm<<<dim3(ch.ntile, (p->NPQ + MG_COLS - 1) / MG_COLS), 128, 0, s>>>(
+      p->d_tiles + ch.tile0, p->n_nodes, p->ldA, p->L_f, p->NPQ, p->d_A, p->d_itab, p->d_lamh,
+      p->d_pq, p->d_U);
+  CKL();
+  record(p, 2);
+  CoupleParams prm{};
+  prm.U = p->d_U;
+  prm.W = p->d_W;
+  prm.out = p->d_out;
+  prm.partials = p->d_partials;
+  prm.comps = comps;
+  prm.count = ch.count;
+  prm.L = p->L_h;
+  prm.n = p->n;
+  prm.nb = p->nb;
+  prm.ncol = p->ncol;
+  prm.NPQ = p->NPQ;
+  prm.n_col_tiles = p->n_col_tiles;
+  prm.vol = p->vol;
+  prm.mirror = p->mirror;
+  prm.qoff = p->d_qoff;
+  prm.rou = p->d_rou;
+  prm.perm = p->d_perm;
+  prm.phase = p->d_phase;
+  prm.betaw = p->d_betaw;
+  prm.fft = p->fft;
+  prm.generic_dft = p->generic_dft;
+  const int MT = 8 * p->MG;
+  dim3 grid(p->n_col_tiles, (ch.count + MT - 1) / MT);
+  launch_couple(p->MG, p->NG, prm, grid, p->couple_smem, s);
+  CKL();
+  record(p, 3);
+  k_digest<<<(ch.count + 127) / 128, 128, 0, s>>>(comps, ch.count, p->n_col_tiles, p->n,
+                                                  p->d_partials, p->mirror, p->d_digest);
+  CKL();
+  record(p, 4);
+  p->launches += 4;
+  if (p->profile) {
+    accumulate(p, ST_LEGENDRE, 0, 1);
+    accumulate(p, ST_MODGEMM, 1, 2);
+    accumulate(p, ST_COUPLE, 2, 3);
+    accumulate(p, ST_DIGEST, 3, 4);
+  }
+}
+
+void load_inputs(slsht_cuda_plan* p, const double* f, const double* h, bool on_device) {
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CK(cudaMemcpyAsync(p->d_f, f, sizeof(double) * 2 * coeff_count(p->L_f), kind, p->stream));
+  CK(cudaMemcpyAsync(p->d_h, h, sizeof(double) * 2 * coeff_count(p->L_h), kind, p->stream));
+}
+
+void check_numeric(slsht_cuda_plan* p) {
+  int flag = 0;
+  CK(cudaMemcpyAsync(&flag, p->d_err, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  if (flag == 1) throw Status{SLSHT_ERR_NUMERIC, "theta weight imaginary residue exceeds 1e-12"};
+  if (flag == 2) throw Status{SLSHT_ERR_NUMERIC, "beta weight imaginary residue exceeds 1e-12"};
+}
+
+template <class F>
+int guarded(slsht_cuda_plan* p, F&& fn) {
+  try {
+    if (p) CK(cudaSetDevice(p->desc.device));
+    fn();
+    return SLSHT_OK;
+  } catch (const Status& st) {
+    if (p) p->last_error = st.msg;
+    else g_create_error = st.msg;
+    return st.code;
+  } catch (const CudaError& e) {
+    if (p) p->last_error = e.msg;
+    else g_create_error = e.msg;
+    return SLSHT_ERR_DEVICE;
+  } catch (const std::exception& e) {
+    if (p) p->last_error = e.what();
+    else g_create_error = e.what();
+    return SLSHT_ERR_DEVICE;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int slsht_cuda_plan_create(const slsht_cuda_desc* desc, slsht_cuda_plan** out) {
+  if (!desc || !out) {
+    g_create_error = "null argument";
+    return SLSHT_ERR_VALIDATION;
+  }
+  *out = nullptr;
+  slsht_cuda_plan* p = new slsht_cuda_plan();
+  p->desc = *desc;
+  int rc = SLSHT_OK;
+  try {
+    build_plan(p);
+  } catch (const Status& st) {
+    g_create_error = st.msg;
+    rc = st.code;
+  } catch (const CudaError& e) {
+    g_create_error = e.msg;
+    rc = SLSHT_ERR_DEVICE;
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    rc = SLSHT_ERR_DEVICE;
+  }
+  if (rc != SLSHT_OK) {
+    free_plan(p);
+    return rc;
+  }
+  *out = p;
+  return SLSHT_OK;
+}
+
+void slsht_cuda_plan_destroy(slsht_cuda_plan* p) {
+  if (p) cudaSetDevice(p->desc.device);
+  free_plan(p);
+}
+
+const char* slsht_cuda_last_error(const slsht_cuda_plan* p) {
+  return p ? p->last_error.c_str() : g_create_error.c_str();
+}
+
+int slsht_cuda_forward_device(slsht_cuda_plan* p, const double* f, const double* h,
+                              int inputs_on_device, double* digests, int digests_on_device,
+                              int synchronize) {
+  if (!p) return SLSHT_ERR_VALIDATION;
+  return guarded(p, [&] {
+    if (!synchronize && digests && !digests_on_device)
+      throw Status{SLSHT_ERR_VALIDATION, "asynchronous forward needs device digests"};
+    p->launches = 0;
+    for (double& v : p->stage_ms) v = 0.0;
+    load_inputs(p, f, h, inputs_on_device != 0);
+    run_setup(p);
+    for (const Chunk& ch : p->chunks) run_chunk(p, ch);
+    if (digests) {
+      const size_t bytes = (size_t)p->digest_rows * 8 * sizeof(double);
+      CK(cudaMemcpyAsync(digests, p->d_digest, bytes,
+                         digests_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                         p->stream));
+    }
+    if (synchronize) check_numeric(p);
+  });
+}
+
+int slsht_cuda_forward(slsht_cuda_plan* p, const double* f, const double* h, slsht_host_sink sink,
+                       void* user) {
+  if (!p) return SLSHT_ERR_VALIDATION;
+  return guarded(p, [&] {
+    if (p->materialize)
+      throw Status{SLSHT_ERR_VALIDATION, "host-sink forward needs a streaming (ring) plan"};
+    p->launches = 0;
+    for (double& v : p->stage_ms) v = 0.0;
+    const int per = p->mirror ? 2 : 1;
+    const size_t chunk_bytes = (size_t)per * p->max_chunk * p->vol * 16;
+    if (p->stage_bytes < chunk_bytes) {
+      for (int i = 0; i < 2; ++i) {
+        if (p->h_stage[i]) cudaFreeHost(p->h_stage[i]);
+        p->h_stage[i] = nullptr;
+        CK(cudaMallocHost(&p->h_stage[i], chunk_bytes));
+      }
+      p->stage_bytes = chunk_bytes;
+    }
+    load_inputs(p, f, h, false);
+    run_setup(p);
+    check_numeric(p);
+    const size_t vb = (size_t)p->vol * 16;
+    auto deliver = [&](size_t ci) {
+      const Chunk& ch = p->chunks[ci];
+      CK(cudaEventSynchronize(p->ev_copied[ch.buf]));
+      const double2* base = p->h_stage[ch.buf];
+      for (int k = 0; k < ch.count; ++k) {
+        const CompRec& r = p->comps[ch.comp0 + k];
+        sink(r.l, r.m, reinterpret_cast<const double*>(base + (size_t)k * p->vol), user);
+        if (r.mslot >= 0)
+          sink(r.l, -r.m,
+               reinterpret_cast<const double*>(base + (size_t)(p->max_chunk + k) * p->vol), user);
+      }
+    };
+    for (size_t ci = 0; ci < p->chunks.size(); ++ci) {
+      const Chunk& ch = p->chunks[ci];
+      // the ring half and host stage of this chunk were last used by chunk ci-2
+      if (ci >= 2) deliver(ci - 2);
+      CK(cudaStreamWaitEvent(p->stream, p->ev_copied[ch.buf], 0));
+      run_chunk(p, ch);
+      CK(cudaEventRecord(p->ev_done[ch.buf], p->stream));
+      CK(cudaStreamWaitEvent(p->copy_stream, p->ev_done[ch.buf], 0));
+      const double2* src = p->d_out + (size_t)ch.buf * per * p->max_chunk * p->vol;
+      CK(cudaMemcpyAsync(p->h_stage[ch.buf], src, (size_t)ch.count * vb, cudaMemcpyDeviceToHost,
+                         p->copy_stream));
+      if (per == 2)
+        CK(cudaMemcpyAsync(p->h_stage[ch.buf] + (size_t)p->max_chunk * p->vol,
+                           src + (size_t)p->max_chunk * p->vol, (size_t)ch.count * vb,
+                           cudaMemcpyDeviceToHost, p->copy_stream));
+      CK(cudaEventRecord(p->ev_copied[ch.buf], p->copy_stream));
+    }
+    const size_t nc = p->chunks.size();
+    if (nc >= 2) deliver(nc - 2);
+    if (nc >= 1) deliver(nc - 1);
+    CK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+const double* slsht_cuda_device_output(const slsht_cuda_plan* p) {
+  return (p && p->materialize) ? reinterpret_cast<const double*>(p->d_out) : nullptr;
+}
+long long slsht_cuda_volume_elems(const slsht_cuda_plan* p) { return p ? p->vol : 0; }
+long long slsht_cuda_computed_count(const slsht_cuda_plan* p) {
+  return p ? (long long)p->comps.size() : 0;
+}
+long long slsht_cuda_emitted_count(const slsht_cuda_plan* p) { return p ? p->emitted : 0; }
+void* slsht_cuda_stream(const slsht_cuda_plan* p) { return p ? (void*)p->stream : nullptr; }
+long long slsht_cuda_launch_count(const slsht_cuda_plan* p) { return p ? p->launches : 0; }
+
+int slsht_cuda_stage_times(const slsht_cuda_plan* p, double* out_ms, int n) {
+  if (!p || !out_ms) return 0;
+  const int k = std::min(n, (int)ST_COUNT);
+  for (int i = 0; i < k; ++i) out_ms[i] = p->stage_ms[i];
+  return k;
+}
+
+int slsht_cuda_delta_tables(int device, int L, double* out) {
+  slsht_cuda_plan* none = nullptr;
+  (void)none;
+  try {
+    if (L < 0) throw Status{SLSHT_ERR_VALIDATION, "band limit must be non-negative"};
+    int dev_count = 0;
+    if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+      throw Status{SLSHT_ERR_DEVICE, "no CUDA device available (the engine has no CPU fallback)"};
+    CK(cudaSetDevice(device));
+    size_t dsz = 0;
+    for (int pp = 0; pp <= L; ++pp) dsz += (size_t)(2 * pp + 1) * (2 * pp + 1);
+    double* d = dalloc<double>(dsz);
+    const size_t dsm = sizeof(double) * ((size_t)(L + 1) * (L + 1) + (L + 1));
+    k_delta<<<1, 128, dsm>>>(L, d);
+    CKL();
+    CK(cudaMemcpy(out, d, dsz * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaFree(d));
+    return SLSHT_OK;
+  } catch (const Status& st) {
+    g_create_error = st.msg;
+    return st.code;
+  } catch (const CudaError& e) {
+    g_create_error = e.msg;
+    return SLSHT_ERR_DEVICE;
+  }
+}
+
+int slsht_cuda_modulated(slsht_cuda_plan* p, const double* f, int count, const int* l,
+                         const int* m, double* out) {
+  if (!p) return SLSHT_ERR_VALIDATION;
+  return guarded(p, [&] {
+    for (int i = 0; i < count; ++i)
+      if (std::abs(m[i]) > l[i] || l[i] > p->L_g)
+        throw Status{SLSHT_ERR_VALIDATION, "modulated transform requires |m| <= l <= L_f+L_h"};
+    // one segment / tile per requested component (rows are independent)
+    std::vector<Seg> segs;
+    std::vector<MTile> tiles;
+    for (int i = 0; i < count; ++i) {
+      segs.push_back(Seg{m[i], l[i], l[i], i});
+      tiles.push_back(MTile{m[i], i, 1});
+    }
+    cudaStream_t s = p->stream;
+    CK(cudaMemcpyAsync(p->d_f, f, sizeof(double) * 2 * coeff_count(p->L_f), cudaMemcpyHostToDevice, s));
+    run_setup(p);
+    Seg* ds = dupload(segs, s);
+    MTile* dt = dupload(tiles, s);
+    double* A = dalloc<double>((size_t)count * p->ldA);
+    double2* U = dalloc<double2>((size_t)count * p->NPQ);
+    k_agen<<<dim3(count, (p->ldA + 127) / 128), 128, 0, s>>>(ds, p->n_nodes, p->ldA, p->d_ncos,
+                                                             p->d_nsin, p->d_weights, A);
+    CKL();
+    k_modgemm<<<dim3(count, (p->NPQ + MG_COLS - 1) / MG_COLS), 128, 0, s>>>(
+        dt, p->n_nodes, p->ldA, p->L_f, p->NPQ, A, p->d_itab, p->d_lamh, p->d_pq, U);
+    CKL();
+    std::vector<double2> hU((size_t)count * p->NPQ);
+    CK(cudaMemcpyAsync(hU.data(), U, hU.size() * 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(ds);
+    cudaFree(dt);
+    cudaFree(A);
+    cudaFree(U);
+    // back to the reference's triangular coeff_index(p, q) order, un-conjugated
+    const int L = p->L_h;
+    for (int i = 0; i < count; ++i) {
+      int c = 0;
+      for (int q = -L; q <= L; ++q)
+        for (int pp = std::abs(q); pp <= L; ++pp, ++c) {
+          const double2 v = hU[(size_t)i * p->NPQ + c];
+          double* o = out + 2 * ((size_t)i * p->NPQ + coeff_index(pp, q));
+          o[0] = v.x;
+          o[1] = -v.y;
+        }
+    }
+  });
+}
+
+}  // extern "C"

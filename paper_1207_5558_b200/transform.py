@@ -1,0 +1,268 @@
+"""Host-side mirror of the reference's forward_fast interface over the C ABI.
+
+Names, argument meaning and error behaviour follow /root/reference/proj/include/slsht:
+  * SphCoeffs            harmonics.hpp:18-33   (coeff_index(l, m) = l*l + l + m)
+  * So3Volume layout     transform.hpp:13-29   ((a*(L_h+1)+b)*n + c, n = 2 L_h + 1)
+  * ForwardOptions       transform.hpp:145-157
+  * forward_fast (x2)    transform.hpp:159-165, transform.cpp:244-311
+  * ValidationError / NumericError  errors.hpp:7-16
+Every call runs the sm_100a kernels of libslsht_cuda.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+
+class ValidationError(ValueError):
+    """slsht::ValidationError (std::invalid_argument); CLI exit code 2."""
+
+
+class NumericError(ArithmeticError):
+    """slsht::NumericError (std::runtime_error); CLI exit code 3."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA runtime failure or no sm_100a device (status 4)."""
+
+
+def coeff_index(l: int, m: int) -> int:
+    return l * l + l + m
+
+
+def coeff_count(band_limit: int) -> int:
+    return (band_limit + 1) * (band_limit + 1)
+
+
+def volume_shape(L_h: int) -> tuple[int, int, int]:
+    n = 2 * L_h + 1
+    return (n, L_h + 1, n)
+
+
+@dataclass
+class SphCoeffs:
+    band_limit: int
+    data: np.ndarray
+    real_signal: bool = False
+
+    @staticmethod
+    def zeros(band_limit: int, real_signal: bool = False) -> "SphCoeffs":
+        return SphCoeffs(band_limit, np.zeros(coeff_count(band_limit), np.complex128), real_signal)
+
+    def at(self, l: int, m: int) -> complex:
+        return complex(self.data[coeff_index(l, m)])
+
+    def __post_init__(self):
+        self.data = np.ascontiguousarray(self.data, dtype=np.complex128)
+        if self.data.size != coeff_count(self.band_limit):
+            raise ValidationError("coefficient array size does not match the band limit")
+
+
+@dataclass
+class ForwardOptions:
+    lmax: int = -1
+    threads: int = 0
+    use_real_symmetry: bool = True
+    emit_negative_m: bool = True
+
+
+@dataclass
+class SlshtDistribution:
+    L_f: int
+    L_h: int
+    L_g: int
+    lmax: int
+    components: np.ndarray = field(repr=False)  # [coeff_count(lmax), n, L_h+1, n]
+
+    def component(self, l: int, m: int) -> np.ndarray:
+        return self.components[coeff_index(l, m)]
+
+
+def _raise(code: int, plan) -> None:
+    if code == L.SLSHT_OK:
+        return
+    lib = L.load()
+    msg = lib.slsht_cuda_last_error(plan).decode(errors="replace")
+    if code == L.SLSHT_ERR_VALIDATION:
+        raise ValidationError(msg)
+    if code == L.SLSHT_ERR_NUMERIC:
+        raise NumericError(msg)
+    raise DeviceError(msg)
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class Plan:
+    """Owns one slsht_cuda_plan (device tables, chunk schedule, output ring or buffer)."""
+
+    def __init__(self, L_f: int, L_h: int, *, lmax: int = -1, real_mode: bool = False,
+                 emit_negative_m: bool = True, device: int = 0, l_begin: int = 0,
+                 l_end: int = -1, materialize: bool = False, ring_bytes: int = 0,
+                 stream: int | None = None):
+        self.lib = L.load()
+        d = L.slsht_cuda_desc()
+        d.L_f, d.L_h, d.lmax = L_f, L_h, lmax
+        d.real_mode, d.emit_negative_m = int(real_mode), int(emit_negative_m)
+        d.device, d.l_begin, d.l_end = device, l_begin, l_end
+        d.materialize, d.ring_bytes = int(materialize), int(ring_bytes)
+        d.stream = stream
+        handle = C.c_void_p()
+        rc = self.lib.slsht_cuda_plan_create(C.byref(d), C.byref(handle))
+        _raise(rc, None)
+        self.handle = handle
+        self.L_f, self.L_h = L_f, L_h
+        self.lmax = (L_f + L_h) if lmax < 0 else lmax
+        self.real_mode = real_mode
+        self.materialize = materialize
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.lib.slsht_cuda_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- queries
+    @property
+    def volume_elems(self) -> int:
+        return int(self.lib.slsht_cuda_volume_elems(self.handle))
+
+    @property
+    def computed_count(self) -> int:
+        return int(self.lib.slsht_cuda_computed_count(self.handle))
+
+    @property
+    def emitted_count(self) -> int:
+        return int(self.lib.slsht_cuda_emitted_count(self.handle))
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.slsht_cuda_stream(self.handle) or 0)
+
+    @property
+    def device_output(self) -> int:
+        return int(self.lib.slsht_cuda_device_output(self.handle) or 0)
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.slsht_cuda_launch_count(self.handle))
+
+    def stage_times(self) -> list[float]:
+        out = (C.c_double * 8)()
+        k = self.lib.slsht_cuda_stage_times(self.handle, out, 8)
+        return list(out[:k])
+
+    # ---- compute
+    def forward_device(self, f_ptr: int, h_ptr: int, *, inputs_on_device: bool,
+                       digests_ptr: int | None, digests_on_device: bool,
+                       synchronize: bool = True) -> None:
+        rc = self.lib.slsht_cuda_forward_device(self.handle, C.c_void_p(f_ptr), C.c_void_p(h_ptr),
+                                                int(inputs_on_device),
+                                                C.c_void_p(digests_ptr or 0),
+                                                int(digests_on_device), int(synchronize))
+        _raise(rc, self.handle)
+
+    def forward_digests(self, f: np.ndarray, h: np.ndarray) -> np.ndarray:
+        """Host f, h -> host digests [coeff_count(lmax), 8] (NaN rows not in this plan)."""
+        f = np.ascontiguousarray(f, np.complex128)
+        h = np.ascontiguousarray(h, np.complex128)
+        dig = np.full((coeff_count(self.lmax), L.DIGEST_WIDTH), np.nan)
+        self.forward_device(f.ctypes.data, h.ctypes.data, inputs_on_device=False,
+                            digests_ptr=dig.ctypes.data, digests_on_device=False)
+        return dig
+
+    def forward_sink(self, f: np.ndarray, h: np.ndarray, sink) -> None:
+        """Stream every emitted component to sink(l, m, volume) (volume valid during the call)."""
+        f = np.ascontiguousarray(f, np.complex128)
+        h = np.ascontiguousarray(h, np.complex128)
+        shape = volume_shape(self.L_h)
+        count = int(np.prod(shape))
+        err: list[BaseException] = []
+
+        def cb(l, m, ptr, _user):
+            if err:
+                return
+            try:
+                vol = np.ctypeslib.as_array(ptr, shape=(2 * count,)).view(np.complex128)
+                sink(l, m, vol.reshape(shape))
+            except BaseException as e:  # re-raised after the C call returns
+                err.append(e)
+
+        cfn = L.SINK(cb)
+        rc = self.lib.slsht_cuda_forward(self.handle, _dptr(f), _dptr(h), cfn, None)
+        if err:
+            raise err[0]
+        _raise(rc, self.handle)
+
+
+def _real_mode(f: SphCoeffs, h: SphCoeffs, opts: ForwardOptions) -> bool:
+    # transform.cpp:253-254
+    return bool(opts.use_real_symmetry and f.real_signal and h.real_signal)
+
+
+def forward_fast(f: SphCoeffs, h: SphCoeffs, sink=None, opts: ForwardOptions | None = None,
+                 *, device: int = 0, ring_bytes: int = 1 << 28):
+    """slsht::forward_fast on the B200.
+
+    With a sink: every component (l, m) is delivered once as sink(l, m, volume[n, L_h+1, n]);
+    calls are serialized; in real mode (l, -m) follows (l, m) (transform.cpp:280-284).
+    Without a sink: returns the materialized SlshtDistribution (transform.cpp:297-311).
+    """
+    opts = opts or ForwardOptions()
+    L_f, L_h = f.band_limit, h.band_limit
+    L_g = L_f + L_h
+    lmax = L_g if opts.lmax < 0 else opts.lmax
+    if lmax > L_g:  # transform.cpp:250-252
+        raise ValidationError("fast engine computes components up to L_f + L_h only")
+    with Plan(L_f, L_h, lmax=lmax, real_mode=_real_mode(f, h, opts),
+              emit_negative_m=opts.emit_negative_m, device=device, materialize=False,
+              ring_bytes=ring_bytes) as plan:
+        if sink is not None:
+            plan.forward_sink(f.data, h.data, sink)
+            return None
+        comps = np.zeros((coeff_count(lmax),) + volume_shape(L_h), np.complex128)
+
+        def store(l, m, vol):
+            comps[coeff_index(l, m)] = vol
+
+        plan.forward_sink(f.data, h.data, store)
+        return SlshtDistribution(L_f, L_h, L_g, lmax, comps)
+
+
+def delta_tables(band_limit: int, device: int = 0) -> np.ndarray:
+    """Delta^p = d^p(pi/2), p <= band_limit, flat in the reference's layout (wigner.hpp:20-30)."""
+    lib = L.load()
+    size = sum((2 * p + 1) ** 2 for p in range(band_limit + 1))
+    out = np.zeros(size)
+    rc = lib.slsht_cuda_delta_tables(device, band_limit, out.ctypes.data_as(L._dp))
+    _raise(rc, None)
+    return out
+
+
+def modulated_sht(f: SphCoeffs, lm: list[tuple[int, int]], window_band_limit: int,
+                  device: int = 0) -> np.ndarray:
+    """ModulatedSht::compute for several (l, m): [len(lm), coeff_count(L_h)] complex."""
+    with Plan(f.band_limit, window_band_limit, device=device, lmax=0, ring_bytes=1 << 24) as plan:
+        ls = (C.c_int * len(lm))(*[l for l, _ in lm])
+        ms = (C.c_int * len(lm))(*[m for _, m in lm])
+        out = np.zeros((len(lm), coeff_count(window_band_limit)), np.complex128)
+        rc = plan.lib.slsht_cuda_modulated(plan.handle, _dptr(f.data), len(lm), ls, ms,
+                                           out.ctypes.data_as(L._dp))
+        _raise(rc, plan.handle)
+        return out
