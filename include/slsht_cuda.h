@@ -98,11 +98,15 @@ long long slsht_cuda_emitted_count(const slsht_cuda_plan* plan);
 void* slsht_cuda_stream(const slsht_cuda_plan* plan);
 
 /* Kernel launches issued by the last forward call, and per-stage device time (ms, CUDA
- * events on the plan stream) when SLSHT_CUDA_PROFILE=1 was set at plan creation:
+ * events on the plan stream) when profiling is on (slsht_cuda_set_profiling, or
+ * SLSHT_CUDA_PROFILE=1 at plan creation):
  * out[0] setup tables, [1] Legendre rows, [2] modulated-SHT GEMM, [3] coupling + alpha FFT
  * + epilogue, [4] digest reduction. Returns the number of entries written. */
 long long slsht_cuda_launch_count(const slsht_cuda_plan* plan);
 int slsht_cuda_stage_times(const slsht_cuda_plan* plan, double* out_ms, int n);
+/* Turn per-stage event timing on or off for subsequent forward calls (adds one host
+ * synchronization per chunk while on). */
+int slsht_cuda_set_profiling(slsht_cuda_plan* plan, int enable);
 
 /* Component-level entry points (host arrays in/out), mirroring the reference's
  * DeltaTables (wigner.cpp:28-80), ModulatedSht::compute (transform.cpp:189-220) and the

@@ -33,6 +33,7 @@ EXPORTS = [
     "slsht_cuda_stream",
     "slsht_cuda_launch_count",
     "slsht_cuda_stage_times",
+    "slsht_cuda_set_profiling",
     "slsht_cuda_delta_tables",
     "slsht_cuda_modulated",
 ]
@@ -93,6 +94,8 @@ def load() -> C.CDLL:
     lib.slsht_cuda_stream.restype = C.c_void_p
     lib.slsht_cuda_stage_times.argtypes = [C.c_void_p, _dp, C.c_int]
     lib.slsht_cuda_stage_times.restype = C.c_int
+    lib.slsht_cuda_set_profiling.argtypes = [C.c_void_p, C.c_int]
+    lib.slsht_cuda_set_profiling.restype = C.c_int
     lib.slsht_cuda_delta_tables.argtypes = [C.c_int, C.c_int, _dp]
     lib.slsht_cuda_delta_tables.restype = C.c_int
     lib.slsht_cuda_modulated.argtypes = [C.c_void_p, C.c_void_p, C.c_int, _ip, _ip, _dp]

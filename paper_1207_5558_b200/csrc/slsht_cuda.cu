@@ -693,6 +693,12 @@ long long slsht_cuda_emitted_count(const slsht_cuda_plan* p) { return p ? p->emi
 void* slsht_cuda_stream(const slsht_cuda_plan* p) { return p ? (void*)p->stream : nullptr; }
 long long slsht_cuda_launch_count(const slsht_cuda_plan* p) { return p ? p->launches : 0; }
 
+int slsht_cuda_set_profiling(slsht_cuda_plan* p, int enable) {
+  if (!p) return SLSHT_ERR_VALIDATION;
+  p->profile = enable != 0;
+  return SLSHT_OK;
+}
+
 int slsht_cuda_stage_times(const slsht_cuda_plan* p, double* out_ms, int n) {
   if (!p || !out_ms) return 0;
   const int k = std::min(n, (int)ST_COUNT);

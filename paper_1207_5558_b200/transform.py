@@ -163,6 +163,9 @@ class Plan:
     def launch_count(self) -> int:
         return int(self.lib.slsht_cuda_launch_count(self.handle))
 
+    def set_profiling(self, enable: bool) -> None:
+        self.lib.slsht_cuda_set_profiling(self.handle, int(enable))
+
     def stage_times(self) -> list[float]:
         out = (C.c_double * 8)()
         k = self.lib.slsht_cuda_stage_times(self.handle, out, 8)
