@@ -1,0 +1,196 @@
+// Per-chunk kernels around the coupling stage: Legendre rows, the modulated-SHT GEMM on the
+// FP64 tensor cores, and the deterministic digest reduction.
+#pragma once
+
+#include "common.cuh"
+
+namespace slsht_cuda {
+
+// ---------------------------------------------------------------------------------------------
+// A[row][j] = w_j lambda_l^m(theta_j) for the rows l0..l1 of one order-m segment.
+// grid (segments, node blocks of 128); dynamic smem 3 (L_g+1) doubles of recursion coefficients.
+struct Seg {
+  int m, l0, l1, row0;
+};
+
+__global__ void __launch_bounds__(128) k_agen(const Seg* __restrict__ segs, int L_g, int n_nodes,
+                                              int ldA, const double* __restrict__ ncos,
+                                              const double* __restrict__ nsin,
+                                              const double* __restrict__ weights,
+                                              double* __restrict__ A) {
+  extern __shared__ double coef[];
+  double *sf = coef, *ca = coef + (L_g + 1), *cb = coef + 2 * (L_g + 1);
+  const Seg s = segs[blockIdx.x];
+  const int am = s.m < 0 ? -s.m : s.m;
+  legendre_coeffs(am, s.l1, sf, ca, cb);
+  __syncthreads();
+  const int j = blockIdx.y * blockDim.x + threadIdx.x;
+  if (j >= ldA) return;
+  if (j >= n_nodes) {
+    for (int l = s.l0; l <= s.l1; ++l) A[(size_t)(s.row0 + l - s.l0) * ldA + j] = 0.0;
+    return;
+  }
+  const double wj = weights[j];
+  LegendreIt r;
+  r.seed(s.m, ncos[j], nsin[j], sf);
+  while (r.l < s.l0) r.next(ca, cb);
+  for (int l = s.l0; l <= s.l1; ++l) {
+    if (l > s.l0) r.next(ca, cb);
+    A[(size_t)(s.row0 + l - s.l0) * ldA + j] = wj * r.cur;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// The modulated SHT (transform.cpp:189-220) of every row of one order m as a GEMM on the FP64
+// tensor cores:
+//   mod[row][c] = sum_j A[row][j] * B_m[j][c],  B_m[j][c] = I(theta_j, m - q_c) lambda_c(theta_j)
+// (zero where |m - q_c| > L_f), c in q-major (p, q) order. U = conj(mod) is stored.
+// CTA tile 32 rows x 64 complex columns, K chunks of 32 nodes; B_m is generated on the fly
+// into shared memory and reused by the 32 rows. 8 warps = 2 row groups x 4 column groups,
+// each warp 16 rows x 16 complex columns = 8 DMMA per k-step of 4.
+struct MTile {
+  int m, row0, rows;
+};
+
+constexpr int MG_ROWS = 32;  // rows per CTA tile
+constexpr int MG_COLS = 64;  // complex columns per CTA tile
+constexpr int MG_K = 32;     // nodes per K chunk
+
+__global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles, int n_nodes,
+                                                 int ldA, int L_f, int NPQ,
+                                                 const double* __restrict__ A,
+                                                 const double2* __restrict__ itab,
+                                                 const double* __restrict__ lamh,
+                                                 const int* __restrict__ pq_q,
+                                                 double2* __restrict__ U) {
+  __shared__ double As[MG_ROWS][MG_K + 4];
+  __shared__ double Br[MG_K][MG_COLS + 4];
+  __shared__ double Bi[MG_K][MG_COLS + 4];
+  __shared__ int colq[MG_COLS];
+  const MTile t = tiles[blockIdx.x];
+  const int cbase = blockIdx.y * MG_COLS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rg = warp >> 2, cgp = warp & 3;
+  if (tid < MG_COLS) colq[tid] = (cbase + tid < NPQ) ? pq_q[2 * (cbase + tid)] : 0;
+  double acc[2][2][2][2];  // [row frag][col frag][re/im][e]
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) acc[a][b][c][0] = acc[a][b][c][1] = 0.0;
+  __syncthreads();
+  const int kk = tid & 31;  // node within the chunk handled by this thread in the B build
+  for (int k0 = 0; k0 < ldA; k0 += MG_K) {
+#pragma unroll
+    for (int it = 0; it < MG_ROWS * MG_K / 256; ++it) {
+      const int e = tid + it * 256;
+      const int r = e / MG_K, k = e % MG_K;
+      As[r][k] = (r < t.rows) ? A[(size_t)(t.row0 + r) * ldA + k0 + k] : 0.0;
+    }
+    const int j = k0 + kk;
+#pragma unroll
+    for (int it = 0; it < MG_COLS / 8; ++it) {
+      const int cc = (tid >> 5) + 8 * it;
+      const int c = cbase + cc;
+      double vr = 0.0, vi = 0.0;
+      if (c < NPQ && j < n_nodes) {
+        const int mu = t.m - colq[cc];
+        if (mu >= -L_f && mu <= L_f) {
+          const double2 iv = itab[(size_t)(mu + L_f) * n_nodes + j];
+          const double lv = lamh[(size_t)c * n_nodes + j];
+          vr = iv.x * lv;
+          vi = iv.y * lv;
+        }
+      }
+      Br[kk][cc] = vr;
+      Bi[kk][cc] = vi;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < MG_K / 4; ++ks) {
+      const int k = ks * 4 + (lane & 3);
+      const double a0 = As[rg * 16 + (lane >> 2)][k];
+      const double a1 = As[rg * 16 + 8 + (lane >> 2)][k];
+#pragma unroll
+      for (int cf = 0; cf < 2; ++cf) {
+        const int col = cgp * 16 + cf * 8 + (lane >> 2);
+        const double br = Br[k][col], bi = Bi[k][col];
+        dmma(acc[0][cf][0][0], acc[0][cf][0][1], a0, br);
+        dmma(acc[0][cf][1][0], acc[0][cf][1][1], a0, bi);
+        dmma(acc[1][cf][0][0], acc[1][cf][0][1], a1, br);
+        dmma(acc[1][cf][1][0], acc[1][cf][1][1], a1, bi);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int rf = 0; rf < 2; ++rf) {
+    const int r = rg * 16 + rf * 8 + (lane >> 2);
+    if (r >= t.rows) continue;
+#pragma unroll
+    for (int cf = 0; cf < 2; ++cf)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = cbase + cgp * 16 + cf * 8 + 2 * (lane & 3) + e;
+        if (c < NPQ)
+          U[(size_t)(t.row0 + r) * NPQ + c] = make_double2(acc[rf][cf][0][e], -acc[rf][cf][1][e]);
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Digest of every emitted component from the per-column-tile partials of k_couple: one warp
+// per component, lanes stride the tiles in order, then a fixed shuffle tree (bitwise
+// deterministic for a given plan). Mirrors (real mode) follow exactly from conjugation.
+__global__ void k_digest(const CompRec* __restrict__ comps, int count, int n_col_tiles, int n,
+                         const double* __restrict__ partials, int mirror,
+                         double* __restrict__ digest) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= count) return;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int t = lane; t < n_col_tiles; t += 32) {
+    const double* r = partials + ((size_t)w * n_col_tiles + t) * 8;
+    acc[0] += r[0];
+    acc[1] = fmax(acc[1], r[1]);
+    acc[2] += r[2];
+    acc[3] += r[3];
+    acc[4] += r[4];
+    acc[5] += r[5];
+    acc[6] += r[6];
+    acc[7] += r[7];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double o = __shfl_down_sync(0xffffffffu, acc[k], off);
+      acc[k] = (k == 1) ? fmax(acc[k], o) : acc[k] + o;
+    }
+  }
+  if (lane != 0) return;
+  const CompRec rec = comps[w];
+  acc[1] = sqrt(acc[1]);  // partials carry max |g|^2
+  const double inv = 1.0 / ((double)n * n * n);
+  acc[6] *= inv;
+  acc[7] *= inv;
+  const int l = rec.l, m = rec.m;
+  double* d = digest + (size_t)(l * l + l + m) * 8;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) d[k] = acc[k];
+  if (mirror && m > 0) {
+    const double s = (m & 1) ? -1.0 : 1.0;
+    double* dm = digest + (size_t)(l * l + l - m) * 8;
+    dm[0] = acc[0];
+    dm[1] = acc[1];
+    dm[2] = s * acc[2];
+    dm[3] = -(s * acc[3]);
+    dm[4] = s * acc[4];
+    dm[5] = -(s * acc[5]);
+    dm[6] = s * acc[6];
+    dm[7] = -(s * acc[7]);
+  }
+}
+
+}  // namespace slsht_cuda

@@ -11,7 +11,9 @@
 #include <string>
 #include <vector>
 
-#include "kernels.cuh"
+#include "kernels_chunk.cuh"
+#include "kernels_couple.cuh"
+#include "kernels_setup.cuh"
 #include "slsht_cuda.h"
 
 using namespace slsht_cuda;
@@ -182,39 +184,42 @@ std::vector<int> factor_odd(int n) {
 // Tile shape of k_couple per transform length: the CTA keeps 8*MG x 8*NG x n complex of T in
 // shared memory (<= ~135 KB), DESIGN.md §3.3.
 void couple_tile(int n, int& MG, int& NG) {
-  if (n <= 33) {
-    MG = 2;
-    NG = 2;
-  } else if (n <= 65) {
-    MG = 2;
-    NG = 1;
-  } else {
-    MG = 1;
-    NG = 1;
-  }
+  MG = n <= 65 ? 2 : 1;
+  NG = n <= 31 ? 2 : 1;
 }
 
 size_t couple_smem_bytes(int n, int MG, int NG) {
-  const size_t T = std::max<size_t>((size_t)64 * MG * NG * n * 16, 256 * 8 * 8);
-  return T + (size_t)n * 16 * 2 + (size_t)((n + 1) & ~1) * 4 + (size_t)(n / 2 + 1) * 8 + 64;
+  return couple_t_bytes(n, MG, NG) + (size_t)n * 32 + (size_t)((n + 1) / 2) * 8 * 2 +
+         (size_t)(2 * n + 1) * 4 + 64;
 }
 
-template <int MG, int NG>
-void set_couple_attr(size_t smem) {
-  CK(cudaFuncSetAttribute(k_couple<MG, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
+using CoupleFn = void (*)(CoupleParams);
+
+// Compile-time instantiations: the BASELINE transform lengths get their own kernel (unrolled
+// FFT plan, only the radices they need); every other odd length takes the runtime-plan kernel.
+CoupleFn couple_kernel(int n, int MG, int NG) {
+  switch (n) {
+    case 17: return k_couple<17, 2, 2, 512, 1>;
+    case 33: return k_couple<33, 2, 1, 256, 2>;
+    case 49: return k_couple<49, 2, 1, 512, 1>;
+    case 65: return k_couple<65, 2, 1, 512, 1>;
+    case 129: return k_couple<129, 1, 1, 256, 1>;
+    default: break;
+  }
+  if (MG == 2 && NG == 2) return k_couple<0, 2, 2, 256, 1>;
+  if (MG == 2 && NG == 1) return k_couple<0, 2, 1, 256, 1>;
+  return k_couple<0, 1, 1, 256, 1>;
 }
 
-template <int MG, int NG>
-void launch_couple_t(const CoupleParams& prm, dim3 grid, size_t smem, cudaStream_t s) {
-  k_couple<MG, NG><<<grid, 256, smem, s>>>(prm);
-}
-
-void launch_couple(int MG, int NG, const CoupleParams& prm, dim3 grid, size_t smem,
-                   cudaStream_t s) {
-  if (MG == 2 && NG == 2) launch_couple_t<2, 2>(prm, grid, smem, s);
-  else if (MG == 2 && NG == 1) launch_couple_t<2, 1>(prm, grid, smem, s);
-  else launch_couple_t<1, 1>(prm, grid, smem, s);
+int couple_threads(int n) {
+  switch (n) {
+    case 17:
+    case 49:
+    case 65:
+      return 512;
+    default:
+      return 256;
+  }
 }
 
 void build_plan(slsht_cuda_plan* p) {
@@ -426,9 +431,8 @@ void build_plan(slsht_cuda_plan* p) {
   p->couple_smem = couple_smem_bytes(p->n, p->MG, p->NG);
   if (p->couple_smem > (size_t)prop.sharedMemPerBlockOptin)
     throw Status{SLSHT_ERR_VALIDATION, "window band limit too large for the shared-memory tile"};
-  if (p->MG == 2 && p->NG == 2) set_couple_attr<2, 2>(p->couple_smem);
-  else if (p->MG == 2 && p->NG == 1) set_couple_attr<2, 1>(p->couple_smem);
-  else set_couple_attr<1, 1>(p->couple_smem);
+  CK(cudaFuncSetAttribute(couple_kernel(p->n, p->MG, p->NG),
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->couple_smem));
   CK(cudaStreamSynchronize(s));
 }
 
@@ -452,10 +456,11 @@ void run_setup(slsht_cuda_plan* p) {
   k_nodes<<<(p->n_nodes + 127) / 128, 128, 0, s>>>(p->N, p->d_ncos, p->d_nsin, p->d_weights, L,
                                                    p->d_betaw, p->d_err);
   CKL();
-  k_legendre_window<<<dim3((p->n_nodes + 127) / 128, p->n), 128, 0, s>>>(
+  k_legendre_window<<<dim3((p->n_nodes + 127) / 128, p->n), 128, 3 * (L + 1) * sizeof(double), s>>>(
       L, p->n_nodes, p->d_ncos, p->d_nsin, p->d_qoff, p->d_lamh);
   CKL();
-  k_itab<<<dim3((p->n_nodes + 127) / 128, 2 * p->L_f + 1), 128, 0, s>>>(
+  k_itab<<<dim3((p->n_nodes + 127) / 128, 2 * p->L_f + 1), 128,
+           3 * (p->L_f + 1) * sizeof(double), s>>>(
       p->L_f, p->n_nodes, p->d_ncos, p->d_nsin, p->d_f, reinterpret_cast<double*>(p->d_itab));
   CKL();
   const size_t dsm = sizeof(double) * ((size_t)(L + 1) * (L + 1) + (L + 1));
@@ -476,11 +481,11 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   cudaStream_t s = p->stream;
   const CompRec* comps = p->d_comps + ch.comp0;
   record(p, 0);
-  k_agen<<<dim3(ch.nseg, (p->ldA + 127) / 128), 128, 0, s>>>(
-      p->d_segs + ch.seg0, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_weights, p->d_A);
+  k_agen<<<dim3(ch.nseg, (p->ldA + 127) / 128), 128, 3 * (p->L_g + 1) * sizeof(double), s>>>(
+      p->d_segs + ch.seg0, p->L_g, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_weights, p->d_A);
   CKL();
   record(p, 1);
-  k_modgemm<<<dim3(ch.ntile, (p->NPQ + MG_COLS - 1) / MG_COLS), 128, 0, s>>>(
+  k_modgemm<<<dim3(ch.ntile, (p->NPQ + MG_COLS - 1) / MG_COLS), 256, 0, s>>>(
       p->d_tiles + ch.tile0, p->n_nodes, p->ldA, p->L_f, p->NPQ, p->d_A, p->d_itab, p->d_lamh,
       p->d_pq, p->d_U);
   CKL();
@@ -509,10 +514,10 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   prm.generic_dft = p->generic_dft;
   const int MT = 8 * p->MG;
   dim3 grid(p->n_col_tiles, (ch.count + MT - 1) / MT);
-  launch_couple(p->MG, p->NG, prm, grid, p->couple_smem, s);
+  couple_kernel(p->n, p->MG, p->NG)<<<grid, couple_threads(p->n), p->couple_smem, s>>>(prm);
   CKL();
   record(p, 3);
-  k_digest<<<(ch.count + 127) / 128, 128, 0, s>>>(comps, ch.count, p->n_col_tiles, p->n,
+  k_digest<<<(ch.count + 3) / 4, 128, 0, s>>>(comps, ch.count, p->n_col_tiles, p->n,
                                                   p->d_partials, p->mirror, p->d_digest);
   CKL();
   record(p, 4);
@@ -754,10 +759,10 @@ int slsht_cuda_modulated(slsht_cuda_plan* p, const double* f, int count, const i
     MTile* dt = dupload(tiles, s);
     double* A = dalloc<double>((size_t)count * p->ldA);
     double2* U = dalloc<double2>((size_t)count * p->NPQ);
-    k_agen<<<dim3(count, (p->ldA + 127) / 128), 128, 0, s>>>(ds, p->n_nodes, p->ldA, p->d_ncos,
-                                                             p->d_nsin, p->d_weights, A);
+    k_agen<<<dim3(count, (p->ldA + 127) / 128), 128, 3 * (p->L_g + 1) * sizeof(double), s>>>(
+        ds, p->L_g, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_weights, A);
     CKL();
-    k_modgemm<<<dim3(count, (p->NPQ + MG_COLS - 1) / MG_COLS), 128, 0, s>>>(
+    k_modgemm<<<dim3(count, (p->NPQ + MG_COLS - 1) / MG_COLS), 256, 0, s>>>(
         dt, p->n_nodes, p->ldA, p->L_f, p->NPQ, A, p->d_itab, p->d_lamh, p->d_pq, U);
     CKL();
     std::vector<double2> hU((size_t)count * p->NPQ);
