@@ -89,6 +89,14 @@ int slsht_cuda_forward_device(slsht_cuda_plan* plan, const double* f, const doub
                               int inputs_on_device, double* digests, int digests_on_device,
                               int synchronize);
 
+/* Device-consumer forward that additionally copies the full volumes of the listed components
+ * (l[i], m[i]) to volumes[i] (host, count x volume_elems complex) right after their chunk
+ * is produced; components outside the plan's range are left untouched and reported by a
+ * SLSHT_ERR_VALIDATION return. digests as in slsht_cuda_forward_device (host, may be NULL). */
+int slsht_cuda_forward_capture(slsht_cuda_plan* plan, const double* f, const double* h,
+                               double* digests, int count, const int* l, const int* m,
+                               double* volumes);
+
 /* Device pointer to the materialized distribution (materialize == 1): coeff_count(lmax)
  * volumes, volume k at offset k * volume_elems complex. NULL in ring mode. */
 const double* slsht_cuda_device_output(const slsht_cuda_plan* plan);

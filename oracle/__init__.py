@@ -62,10 +62,10 @@ class _Lib:
             raise FileNotFoundError(f"{path} not built (run oracle.build())")
         self.lib = C.CDLL(str(path))
         self.prefix = prefix
-        self.lib[f"{prefix}last_error"].restype = C.c_char_p
+        getattr(self.lib, f"{prefix}last_error").restype = C.c_char_p
 
     def err(self) -> str:
-        return self.lib[f"{self.prefix}last_error"]().decode()
+        return getattr(self.lib, f"{self.prefix}last_error")().decode()
 
     def check(self, rc: int) -> None:
         if rc == 2:
@@ -190,6 +190,8 @@ class Reference(_Lib):
                                               C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp]
         L.ref_eigenfunction_window.argtypes = [C.c_double, C.c_double, C.c_int, C.c_int, _dp, _dp]
         L.ref_random_coeffs.argtypes = [C.c_int, C.c_uint64, C.c_int, _dp]
+        L.ref_components.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_int, C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int), _dp]
         L.ref_rotate_coeffs.argtypes = [C.c_int, _dp, C.c_double, C.c_double, C.c_double, _dp]
 
     def delta_tables(self, L: int) -> np.ndarray:
@@ -275,6 +277,17 @@ class Reference(_Lib):
                                           _ptr(np.ascontiguousarray(h, dtype=np.complex128)),
                                           int(h_real), _ptr(out)))
         return out
+
+    def components(self, f, L_f, h, L_h, lm) -> dict:
+        """Volumes of the listed (l, m) through ModulatedSht/build_c_tensor/So3Evaluator."""
+        lm = list(lm)
+        ls = (C.c_int * len(lm))(*[l for l, _ in lm])
+        ms = (C.c_int * len(lm))(*[m for _, m in lm])
+        out = np.zeros((len(lm),) + volume_shape(L_h), dtype=np.complex128)
+        self.check(self.lib.ref_components(L_f, _ptr(np.ascontiguousarray(f, dtype=np.complex128)), L_h,
+                                           _ptr(np.ascontiguousarray(h, dtype=np.complex128)),
+                                           len(lm), ls, ms, _ptr(out)))
+        return {k: out[i] for i, k in enumerate(lm)}
 
     def eigenfunction_window(self, theta_c: float, a: float, L: int, oversample: int = 4):
         out = np.zeros(coeff_count(L), dtype=np.complex128)

@@ -229,6 +229,32 @@ int ref_roundtrip(int L_f, const double* f, int f_real, int L_h, const double* h
   });
 }
 
+// Selected components (l[i], m[i]) through the reference's component-level public API, exactly
+// as its bench_pass does (proj/src/cli.cpp:94-143): one ModulatedSht, DeltaTables and
+// So3Evaluator, then compute -> build_c_tensor -> evaluate per component.
+int ref_components(int L_f, const double* f, int L_h, const double* h, int count, const int* l,
+                   const int* m, double* out) {
+  return guarded([&] {
+    const slsht::SphCoeffs fc = make_coeffs(L_f, f, 0);
+    const slsht::SphCoeffs hc = make_coeffs(L_h, h, 0);
+    const slsht::ModulatedSht ctx(fc, L_h);
+    const slsht::DeltaTables delta(L_h);
+    const slsht::So3Evaluator ev(L_h);
+    slsht::ModulatedSht::Scratch scratch;
+    slsht::So3Evaluator::Scratch es;
+    slsht::ModulatedCoeffs mod;
+    slsht::CTensor c;
+    slsht::So3Volume vol;
+    const std::size_t V = static_cast<std::size_t>(2 * L_h + 1) * (2 * L_h + 1) * (L_h + 1);
+    for (int i = 0; i < count; ++i) {
+      ctx.compute(l[i], m[i], scratch, mod);
+      slsht::build_c_tensor(mod, hc, delta, c);
+      ev.evaluate(c, es, vol);
+      std::memcpy(out + 2 * V * static_cast<std::size_t>(i), vol.values.data(), sizeof(double) * 2 * V);
+    }
+  });
+}
+
 int ref_eigenfunction_window(double theta_c, double a, int L, int oversample,
                              double* out, double* lambda) {
   return guarded([&] {

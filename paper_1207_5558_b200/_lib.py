@@ -26,6 +26,7 @@ EXPORTS = [
     "slsht_cuda_last_error",
     "slsht_cuda_forward",
     "slsht_cuda_forward_device",
+    "slsht_cuda_forward_capture",
     "slsht_cuda_device_output",
     "slsht_cuda_volume_elems",
     "slsht_cuda_computed_count",
@@ -84,6 +85,9 @@ def load() -> C.CDLL:
     lib.slsht_cuda_forward_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                               C.c_void_p, C.c_int, C.c_int]
     lib.slsht_cuda_forward_device.restype = C.c_int
+    lib.slsht_cuda_forward_capture.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                               C.c_int, _ip, _ip, C.c_void_p]
+    lib.slsht_cuda_forward_capture.restype = C.c_int
     lib.slsht_cuda_device_output.argtypes = [C.c_void_p]
     lib.slsht_cuda_device_output.restype = C.c_void_p
     for name in ("slsht_cuda_volume_elems", "slsht_cuda_computed_count",

@@ -536,6 +536,15 @@ void load_inputs(slsht_cuda_plan* p, const double* f, const double* h, bool on_d
   CK(cudaMemcpyAsync(p->d_h, h, sizeof(double) * 2 * coeff_count(p->L_h), kind, p->stream));
 }
 
+// Digest rows of the plan's degree range [l_begin, l_end) are the contiguous rows
+// [l_begin^2, l_end^2) of the coeff_index table; only those are copied out.
+void copy_digests(slsht_cuda_plan* p, double* digests, bool on_device) {
+  const size_t r0 = (size_t)p->l_begin * p->l_begin, r1 = (size_t)p->l_end * p->l_end;
+  if (r1 <= r0) return;
+  CK(cudaMemcpyAsync(digests + 8 * r0, p->d_digest + 8 * r0, (r1 - r0) * 8 * sizeof(double),
+                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, p->stream));
+}
+
 void check_numeric(slsht_cuda_plan* p) {
   int flag = 0;
   CK(cudaMemcpyAsync(&flag, p->d_err, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
@@ -619,13 +628,57 @@ int slsht_cuda_forward_device(slsht_cuda_plan* p, const double* f, const double*
     load_inputs(p, f, h, inputs_on_device != 0);
     run_setup(p);
     for (const Chunk& ch : p->chunks) run_chunk(p, ch);
-    if (digests) {
-      const size_t bytes = (size_t)p->digest_rows * 8 * sizeof(double);
-      CK(cudaMemcpyAsync(digests, p->d_digest, bytes,
-                         digests_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                         p->stream));
-    }
+    if (digests) copy_digests(p, digests, digests_on_device != 0);
     if (synchronize) check_numeric(p);
+  });
+}
+
+int slsht_cuda_forward_capture(slsht_cuda_plan* p, const double* f, const double* h,
+                               double* digests, int count, const int* l, const int* m,
+                               double* volumes) {
+  if (!p) return SLSHT_ERR_VALIDATION;
+  return guarded(p, [&] {
+    // locate every request: (chunk, slot) of the component or of its conjugate mirror
+    struct Req {
+      size_t chunk;
+      long long slot;
+      int i;
+    };
+    std::vector<Req> reqs;
+    for (int i = 0; i < count; ++i) {
+      bool found = false;
+      for (size_t ci = 0; ci < p->chunks.size() && !found; ++ci) {
+        const Chunk& ch = p->chunks[ci];
+        for (int k = 0; k < ch.count; ++k) {
+          const CompRec& r = p->comps[ch.comp0 + k];
+          if (r.l != l[i]) continue;
+          if (r.m == m[i]) {
+            reqs.push_back({ci, r.slot, i});
+            found = true;
+            break;
+          }
+          if (r.mslot >= 0 && -r.m == m[i]) {
+            reqs.push_back({ci, r.mslot, i});
+            found = true;
+            break;
+          }
+        }
+      }
+      if (!found) throw Status{SLSHT_ERR_VALIDATION, "requested component not produced by this plan"};
+    }
+    p->launches = 0;
+    for (double& v : p->stage_ms) v = 0.0;
+    load_inputs(p, f, h, false);
+    run_setup(p);
+    for (size_t ci = 0; ci < p->chunks.size(); ++ci) {
+      run_chunk(p, p->chunks[ci]);
+      for (const Req& r : reqs)
+        if (r.chunk == ci)
+          CK(cudaMemcpyAsync(volumes + 2 * (size_t)r.i * p->vol, p->d_out + (size_t)r.slot * p->vol,
+                             (size_t)p->vol * 16, cudaMemcpyDeviceToHost, p->stream));
+    }
+    if (digests) copy_digests(p, digests, false);
+    check_numeric(p);
   });
 }
 

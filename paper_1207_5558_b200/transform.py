@@ -190,6 +190,20 @@ class Plan:
                             digests_ptr=dig.ctypes.data, digests_on_device=False)
         return dig
 
+    def forward_capture(self, f: np.ndarray, h: np.ndarray, lm) -> tuple[np.ndarray, dict]:
+        """Device-mode forward returning (digests, {(l, m): volume}) for the listed components."""
+        f = np.ascontiguousarray(f, np.complex128)
+        h = np.ascontiguousarray(h, np.complex128)
+        lm = list(lm)
+        dig = np.full((coeff_count(self.lmax), L.DIGEST_WIDTH), np.nan)
+        vols = np.zeros((max(1, len(lm)),) + volume_shape(self.L_h), np.complex128)
+        ls = (C.c_int * max(1, len(lm)))(*[l for l, _ in lm])
+        ms = (C.c_int * max(1, len(lm)))(*[m for _, m in lm])
+        rc = self.lib.slsht_cuda_forward_capture(self.handle, _dptr(f), _dptr(h), _dptr(dig),
+                                                 len(lm), ls, ms, _dptr(vols))
+        _raise(rc, self.handle)
+        return dig, {k: vols[i] for i, k in enumerate(lm)}
+
     def forward_sink(self, f: np.ndarray, h: np.ndarray, sink) -> None:
         """Stream every emitted component to sink(l, m, volume) (volume valid during the call)."""
         f = np.ascontiguousarray(f, np.complex128)
