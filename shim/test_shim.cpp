@@ -1,0 +1,135 @@
+// Drop-in check of the shim: the reference's own library (sources under /root/reference,
+// with transform.cpp compiled as -Dforward_fast=reference_forward_fast so both engines can
+// live in one binary) drives the B200 forward_fast through its UNCHANGED headers:
+//  * engine equivalence against the reference CPU forward_fast (test_transform.cpp:229-262
+//    shapes, real and complex, windows from the reference's eigenfunction_window);
+//  * the streaming contract: every component once, sink == materialized (test_transform.cpp:331-348);
+//  * the reference's InverseAccumulator consuming the shim's stream: acceptance criterion 1
+//    (acceptance_main.cpp:87-107, error < 1e-9);
+//  * ValidationError for lmax > L_f + L_h (transform.cpp:250-252).
+// Prints one PASS/FAIL line per check; exit status 0 iff all pass.
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <map>
+#include <numbers>
+#include <random>
+#include <vector>
+
+#include "slsht/errors.hpp"
+#include "slsht/signals.hpp"
+#include "slsht/transform.hpp"
+#include "slsht/window.hpp"
+
+namespace slsht {
+// the reference's CPU engine, renamed at compile time (see Makefile)
+void reference_forward_fast(const SphCoeffs& f, const SphCoeffs& h, const ComponentSink& sink,
+                            const ForwardOptions& opts);
+SlshtDistribution reference_forward_fast(const SphCoeffs& f, const SphCoeffs& h,
+                                         const ForwardOptions& opts);
+}  // namespace slsht
+
+using namespace slsht;
+using cplx = std::complex<double>;
+
+static int failures = 0;
+static void report(bool ok, const char* name, double value, double limit) {
+  std::printf("%s %-58s %.3e (limit %.0e)\n", ok ? "PASS" : "FAIL", name, value, limit);
+  if (!ok) ++failures;
+}
+
+static SphCoeffs random_complex(int L, std::uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  SphCoeffs c = SphCoeffs::zeros(L);
+  for (auto& v : c.data)
+    v = cplx(static_cast<double>(rng() >> 11) * 0x1.0p-53 - 0.5,
+             static_cast<double>(rng() >> 11) * 0x1.0p-53 - 0.5);
+  return c;
+}
+
+static double max_diff(const SlshtDistribution& a, const SlshtDistribution& b) {
+  double worst = 0.0;
+  for (int l = 0; l <= a.lmax; ++l)
+    for (int m = -l; m <= l; ++m) {
+      const auto& va = a.component(l, m).values;
+      const auto& vb = b.component(l, m).values;
+      if (va.size() != vb.size()) return INFINITY;
+      for (std::size_t i = 0; i < va.size(); ++i) worst = std::max(worst, std::abs(va[i] - vb[i]));
+    }
+  return worst;
+}
+
+int main() {
+  {
+    const SphCoeffs f = random_complex(3, 41), h = random_complex(2, 42);
+    report(max_diff(forward_fast(f, h), reference_forward_fast(f, h, {})) < 1e-12,
+           "complex (L_f, L_h) = (3, 2) vs reference forward_fast",
+           max_diff(forward_fast(f, h), reference_forward_fast(f, h, {})), 1e-12);
+  }
+  {
+    const SphCoeffs f = random_coeffs(6, 43, true);
+    const Window w = eigenfunction_window({0.3, 0.7}, 3, 4);
+    const double d = max_diff(forward_fast(f, w.coeffs), reference_forward_fast(f, w.coeffs, {}));
+    report(d < 1e-12, "real mode (6, 3), eigenfunction window, mirrored m < 0", d, 1e-12);
+    ForwardOptions full;
+    full.use_real_symmetry = false;
+    const double d2 = max_diff(forward_fast(f, w.coeffs, full), reference_forward_fast(f, w.coeffs, {}));
+    report(d2 < 1e-12, "full-m mode vs reference real mode (conjugate symmetry)", d2, 1e-12);
+  }
+  {
+    const SphCoeffs f = random_complex(32, 1), h = random_complex(8, 2);
+    const SlshtDistribution a = forward_fast(f, h);
+    const SlshtDistribution b = reference_forward_fast(f, h, {});
+    double scale = 0.0;
+    for (const auto& c : b.components)
+      for (const auto& v : c.values) scale = std::max(scale, std::abs(v));
+    const double d = max_diff(a, b) / scale;
+    report(d < 1e-10, "config-1 shape (32, 8): eps_inf relative to max |g|", d, 1e-10);
+  }
+  {
+    const SphCoeffs f = random_complex(3, 71), h = random_complex(2, 72);
+    const SlshtDistribution dist = forward_fast(f, h);
+    std::map<std::pair<int, int>, So3Volume> seen;
+    bool once = true;
+    forward_fast(f, h, [&](int l, int m, const So3Volume& v) {
+      once = once && seen.emplace(std::make_pair(l, m), v).second;
+    });
+    double d = 0.0;
+    for (const auto& [key, vol] : seen) {
+      const auto& ref = dist.component(key.first, key.second).values;
+      for (std::size_t i = 0; i < ref.size(); ++i) d = std::max(d, std::abs(vol.values[i] - ref[i]));
+    }
+    const bool ok = once && seen.size() == static_cast<std::size_t>(coeff_count(5)) && d == 0.0;
+    report(ok, "streaming sink sees every component once, == materialized", d, 0.0);
+  }
+  {
+    const Window win18 = eigenfunction_window(
+        {std::numbers::pi / 6.0, std::numbers::pi / 6.0 + std::numbers::pi / 240.0}, 18, 4);
+    double worst = 0.0;
+    for (const int lf : {18, 32}) {
+      const SphCoeffs f = random_coeffs(lf, 100 + lf, true);
+      InverseAccumulator acc(lf, 18, win18.coeffs.at(0, 0), true);
+      ForwardOptions opts;
+      opts.lmax = lf;
+      opts.emit_negative_m = false;
+      forward_fast(f, win18.coeffs, acc.sink(), opts);
+      const SphCoeffs back = acc.finish();
+      for (int i = 0; i < coeff_count(lf); ++i)
+        worst = std::max(worst, std::abs(back.data[i] - f.data[i]));
+    }
+    report(worst < 1e-9, "round trip via the reference InverseAccumulator (L_h = 18)", worst, 1e-9);
+  }
+  {
+    bool threw = false;
+    try {
+      ForwardOptions opts;
+      opts.lmax = 9;
+      forward_fast(random_complex(4, 5), random_complex(3, 6), opts);
+    } catch (const ValidationError&) {
+      threw = true;
+    }
+    report(threw, "lmax > L_f + L_h throws ValidationError", threw ? 0.0 : 1.0, 0.0);
+  }
+  std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ALL PASSED", failures);
+  return failures ? 1 : 0;
+}
