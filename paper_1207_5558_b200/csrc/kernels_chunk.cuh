@@ -62,6 +62,9 @@ __global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles
                                                  const double2* __restrict__ itab,
                                                  const double* __restrict__ lamh,
                                                  const int* __restrict__ pq_q,
+                                                 int u_group, long long u_gs,
+                                                 const int* __restrict__ u_base,
+                                                 const int* __restrict__ u_str,
                                                  double2* __restrict__ U) {
   __shared__ double As[MG_ROWS][MG_K + 4];
   __shared__ double Br[MG_K][MG_COLS + 4];
@@ -133,8 +136,15 @@ __global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = cbase + cgp * 16 + cf * 8 + 2 * (lane & 3) + e;
-        if (c < NPQ)
-          U[(size_t)(t.row0 + r) * NPQ + c] = make_double2(acc[rf][cf][0][e], -acc[rf][cf][1][e]);
+        if (c < NPQ) {
+          const int row = t.row0 + r;
+          // u_group == 0: U[row][c]; else the stage-tiled layout of the warp-specialized
+          // coupling kernel: group row / MT, stage block u_base[c], row stride u_str[c]
+          const size_t dst = u_group ? (size_t)(row / u_group) * u_gs + u_base[c] +
+                                           (size_t)(row % u_group) * u_str[c]
+                                     : (size_t)row * NPQ + c;
+          U[dst] = make_double2(acc[rf][cf][0][e], -acc[rf][cf][1][e]);
+        }
       }
   }
 }

@@ -45,13 +45,14 @@ constexpr int smallest_prime_factor(int n) {
   return n;
 }
 
-// One DIF stage of radix R on sub-transforms of span S (compile-time N).
+// One DIF stage of radix R on sub-transforms of span S (compile-time N), executed by the
+// NTHR threads numbered tid = 0..NTHR-1.
 template <int N, int R, int S, int NT, int PAIRS, int NTHR>
-__device__ __forceinline__ void fft_stage_ct(double2* T, const double2* rou_s) {
+__device__ __forceinline__ void fft_stage_ct(double2* T, const double2* rou_s, int tid) {
   constexpr int MP = S / R;
   constexpr int TOTAL = PAIRS * (N / R);
   double xr[R], xi[R];
-  for (int item = threadIdx.x; item < TOTAL; item += NTHR) {
+  for (int item = tid; item < TOTAL; item += NTHR) {
     const int pair = item % PAIRS;
     const int bfl = item / PAIRS;
     const int blk = bfl / MP, t = bfl % MP;
@@ -78,19 +79,26 @@ __device__ __forceinline__ void fft_stage_ct(double2* T, const double2* rou_s) {
   }
 }
 
+__device__ __forceinline__ void stage_sync(int bar, int count) {
+  if (bar == 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+
+// Full DIF plan: radices = prime factors of N in ascending order (the host's perm matches).
+// bar 0 synchronizes the whole CTA, bar > 0 only the NTHR participating threads.
 template <int N, int S, int NT, int PAIRS, int NTHR>
 struct FftDif {
-  __device__ __forceinline__ static void run(double2* T, const double2* rou_s) {
+  __device__ __forceinline__ static void run(double2* T, const double2* rou_s, int tid, int bar) {
     constexpr int R = smallest_prime_factor(S);
     static_assert(Radix<R>::kSupported, "no generated butterfly for this radix");
-    fft_stage_ct<N, R, S, NT, PAIRS, NTHR>(T, rou_s);
-    __syncthreads();
-    FftDif<N, S / R, NT, PAIRS, NTHR>::run(T, rou_s);
+    fft_stage_ct<N, R, S, NT, PAIRS, NTHR>(T, rou_s, tid);
+    stage_sync(bar, NTHR);
+    FftDif<N, S / R, NT, PAIRS, NTHR>::run(T, rou_s, tid, bar);
   }
 };
 template <int N, int NT, int PAIRS, int NTHR>
 struct FftDif<N, 1, NT, PAIRS, NTHR> {
-  __device__ __forceinline__ static void run(double2*, const double2*) {}
+  __device__ __forceinline__ static void run(double2*, const double2*, int, int) {}
 };
 
 // Runtime-length stage (any odd n whose prime factors have generated butterflies).
@@ -317,7 +325,7 @@ __global__ void __launch_bounds__(NTHR, MINB) k_couple(const CoupleParams P) {
 
   // ---------------- phase 2: alpha FFT over q, in place
   if constexpr (N_CT > 0) {
-    FftDif<N_CT, N_CT, NT, PAIRS, NTHR>::run(T, rou_s);
+    FftDif<N_CT, N_CT, NT, PAIRS, NTHR>::run(T, rou_s, threadIdx.x, 0);
   } else {
     if (!P.generic_dft) fft_runtime(T, NT, n, PAIRS, P.fft, rou_s, NTHR);
   }

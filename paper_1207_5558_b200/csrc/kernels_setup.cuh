@@ -220,13 +220,27 @@ __global__ void k_dtab(int L, const double* __restrict__ delta, const double2* _
 // Window table of the coupling stage: W[c][col] with c = qoff[q+L] + p-|q| and col = b*n + c_g:
 //   W = sum_{q'=-p}^{p} h_p^{q'} d^p_{q q'}(beta_b) e^{-i q' gamma_{c_g}}.
 // Then g(l, m)[a][b][c] = sum_q e^{-i q alpha_a} sum_p conj(mod_p^q) W[c(p,q)][b*n+c].
+// Layout: tile_nt == 0 -> W[c][col]; tile_nt = NT > 0 -> the column-tiled layout of the
+// warp-specialized coupling kernel, W[col / NT][c][swz(c, col % NT)] with the 16-B chunk
+// swizzle of wtile_index(), columns of the last tile beyond ncol zero-filled.
+__host__ __device__ __forceinline__ size_t wtile_index(int c, int col, int NPQ, int NT) {
+  const int cc = col % NT;
+  const int sw = (cc & ~7) | ((cc & 7) ^ ((2 * c) & 7));
+  return ((size_t)(col / NT) * NPQ + c) * NT + sw;
+}
+
 __global__ void k_wtab(int L, const double* __restrict__ h, const double* __restrict__ dtab,
                        const double2* __restrict__ rou, const int* __restrict__ pq_q,
-                       double2* __restrict__ W) {
+                       int tile_nt, int ncol_pad, double2* __restrict__ W) {
   const int n = 2 * L + 1, nb = L + 1, ncol = n * nb;
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
-  if (col >= ncol) return;
+  const int NPQ = (L + 1) * (L + 1);
+  if (col >= ncol_pad) return;
+  if (col >= ncol) {
+    W[wtile_index(c, col, NPQ, tile_nt)] = make_double2(0.0, 0.0);
+    return;
+  }
   const int q = pq_q[2 * c], p = pq_q[2 * c + 1];
   const int b = col / n, cg = col % n;
   const int w = 2 * p + 1;
@@ -243,7 +257,8 @@ __global__ void k_wtab(int L, const double* __restrict__ h, const double* __rest
     ar += tr * z.x - ti * z.y;
     ai += tr * z.y + ti * z.x;
   }
-  W[(size_t)c * ncol + col] = make_double2(ar, ai);
+  const size_t dst = tile_nt ? wtile_index(c, col, NPQ, tile_nt) : (size_t)c * ncol + col;
+  W[dst] = make_double2(ar, ai);
 }
 
 

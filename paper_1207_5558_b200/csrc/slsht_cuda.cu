@@ -13,6 +13,7 @@
 
 #include "kernels_chunk.cuh"
 #include "kernels_couple.cuh"
+#include "kernels_couple_ws.cuh"
 #include "kernels_setup.cuh"
 #include "slsht_cuda.h"
 
@@ -71,6 +72,14 @@ struct Chunk {
 
 enum Stage { ST_SETUP = 0, ST_LEGENDRE, ST_MODGEMM, ST_COUPLE, ST_DIGEST, ST_COUNT };
 
+// Warp-specialized persistent kernels (kernels_couple_ws.cuh) for the BASELINE lengths.
+struct WsKernel {
+  void (*fn)(WsParams);
+  int threads;
+  size_t smem;
+  int MT, NT, RS;
+};
+
 }  // namespace
 
 struct slsht_cuda_plan {
@@ -87,6 +96,13 @@ struct slsht_cuda_plan {
   FftPlan fft{};
   int generic_dft = 0;
   size_t couple_smem = 0;
+  bool use_ws = false;  // warp-specialized persistent coupling kernel for this length
+  WsKernel ws{};
+  WsStages ws_stages{};
+  int num_sms = 0;
+  int* d_ubase = nullptr;  // stage-tiled U layout (ws path): per (p, q) row block offset
+  int* d_ustr = nullptr;   //   and row stride
+  int ct_fast = 0;
   cudaStream_t stream = nullptr, copy_stream = nullptr;
   bool own_stream = false;
   bool profile = false;
@@ -149,6 +165,8 @@ void free_plan(slsht_cuda_plan* p) {
   cudaFree(p->d_perm);
   cudaFree(p->d_qoff);
   cudaFree(p->d_pq);
+  cudaFree(p->d_ubase);
+  cudaFree(p->d_ustr);
   cudaFree(p->d_err);
   cudaFree(p->d_comps);
   cudaFree(p->d_segs);
@@ -211,6 +229,25 @@ CoupleFn couple_kernel(int n, int MG, int NG) {
   return k_couple<0, 1, 1, 256, 1>;
 }
 
+// <N, MG, NG, stage rows, stages, warps per consumer group>
+
+template <int N, int MG, int NG, int RS, int NSTAGE, int GW>
+WsKernel ws_entry() {
+  using Cfg = WsCfg<N, MG, NG, RS, NSTAGE, GW>;
+  return WsKernel{k_couple_ws<N, MG, NG, RS, NSTAGE, GW>, Cfg::NTHREADS, Cfg::SMEM, Cfg::MT,
+                  Cfg::NT, RS};
+}
+
+bool ws_kernel(int n, WsKernel& k) {
+  switch (n) {
+    case 17: k = ws_entry<17, 2, 2, 44, 3, 8>(); return true;
+    case 33: k = ws_entry<33, 2, 1, 56, 3, 8>(); return true;
+    // n = 49, 65, 129 (one 8x8 warp tile) stay on k_couple until the MMA warps of the
+    // persistent kernel can split the k range of one q
+    default: return false;
+  }
+}
+
 int couple_threads(int n) {
   switch (n) {
     case 17:
@@ -250,6 +287,24 @@ void build_plan(slsht_cuda_plan* p) {
   p->ldA = (p->n_nodes + MG_K - 1) / MG_K * MG_K;
   p->vol = (long long)p->n * p->n * p->nb;
   couple_tile(p->n, p->MG, p->NG);
+  if (std::getenv("SLSHT_CUDA_NO_WS") == nullptr && ws_kernel(p->n, p->ws)) {
+    p->use_ws = true;
+    p->MG = p->ws.MT / 8;
+    p->NG = p->ws.NT / 8;
+    // q-groups of consecutive rows jq with at most RS (p, q) rows per operand stage
+    int cnt = 0, rows = 0;
+    p->ws_stages.js[0] = 0;
+    for (int jq = 0; jq < p->n; ++jq) {
+      const int np = L + 1 - std::abs(jq - L);
+      if (rows + np > p->ws.RS) {
+        p->ws_stages.js[++cnt] = jq;
+        rows = 0;
+      }
+      rows += np;
+    }
+    p->ws_stages.js[++cnt] = p->n;
+    p->ws_stages.count = cnt;
+  }
   p->n_col_tiles = (p->ncol + 8 * p->NG - 1) / (8 * p->NG);
   const char* prof = std::getenv("SLSHT_CUDA_PROFILE");
   p->profile = prof && prof[0] == '1';
@@ -282,6 +337,26 @@ void build_plan(slsht_cuda_plan* p) {
       pq[2 * c] = q;
       pq[2 * c + 1] = pp;
     }
+  }
+  // ---- stage-tiled U layout of the warp-specialized coupling kernel: per component group,
+  // stage s holds MT rows of USTR_s (>= the stage's (p, q) rows, == 4 mod 8) complex
+  std::vector<int> ubase(p->NPQ, 0), ustr(p->NPQ, 0);
+  if (p->use_ws) {
+    const int MT = p->ws.MT;
+    long long off = 0;
+    for (int st = 0; st < p->ws_stages.count; ++st) {
+      const int r0 = qoff[p->ws_stages.js[st]], r1 = qoff[p->ws_stages.js[st + 1]];
+      const int rows = r1 - r0;
+      const int us = rows + (((4 - rows) % 8) + 8) % 8;
+      p->ws_stages.uoff[st] = (int)off;
+      p->ws_stages.ustr[st] = us;
+      for (int c = r0; c < r1; ++c) {
+        ubase[c] = (int)off + (c - r0);
+        ustr[c] = us;
+      }
+      off += (long long)MT * us;
+    }
+    p->ws_stages.group_elems = off;
   }
   // ---- alpha-axis FFT plan: roots of unity, DIF stages, output permutation, phase shift
   const int n = p->n;
@@ -399,7 +474,11 @@ void build_plan(slsht_cuda_plan* p) {
   for (int pp = 0; pp <= L; ++pp) dsz += (size_t)(2 * pp + 1) * (2 * pp + 1);
   p->d_delta = dalloc<double>(dsz);
   p->d_dtab = dalloc<double>(dsz * p->nb);
-  p->d_W = dalloc<double2>((size_t)p->NPQ * p->ncol);
+  const size_t ncol_pad = p->use_ws ? (size_t)p->n_col_tiles * p->ws.NT : (size_t)p->ncol;
+  p->d_W = dalloc<double2>((size_t)p->NPQ * ncol_pad);
+  p->ct_fast = (size_t)p->NPQ * ncol_pad * 16 < (48u << 20);
+  p->d_ubase = dupload(ubase, s);
+  p->d_ustr = dupload(ustr, s);
   p->d_rou = dupload(rou, s);
   p->d_phase = dupload(phase, s);
   p->d_perm = dupload(perm, s);
@@ -411,7 +490,12 @@ void build_plan(slsht_cuda_plan* p) {
   p->d_segs = dupload(p->segs, s);
   p->d_tiles = dupload(p->tiles, s);
   p->d_A = dalloc<double>((size_t)p->max_chunk * p->ldA);
-  p->d_U = dalloc<double2>((size_t)p->max_chunk * p->NPQ);
+  if (p->use_ws) {
+    const size_t groups = (size_t)(p->max_chunk + p->ws.MT - 1) / p->ws.MT;
+    p->d_U = dalloc<double2>(groups * (size_t)p->ws_stages.group_elems);
+  } else {
+    p->d_U = dalloc<double2>((size_t)p->max_chunk * p->NPQ);
+  }
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   const size_t out_bytes = (size_t)p->n_slots * vol_bytes;
@@ -428,11 +512,18 @@ void build_plan(slsht_cuda_plan* p) {
   }
   for (auto& e : p->ev_stage) CK(cudaEventCreate(&e));
 
-  p->couple_smem = couple_smem_bytes(p->n, p->MG, p->NG);
+  p->num_sms = prop.multiProcessorCount;
+  if (p->use_ws) {
+    p->couple_smem = p->ws.smem;
+    CK(cudaFuncSetAttribute(p->ws.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)p->couple_smem));
+  } else {
+    p->couple_smem = couple_smem_bytes(p->n, p->MG, p->NG);
+    CK(cudaFuncSetAttribute(couple_kernel(p->n, p->MG, p->NG),
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->couple_smem));
+  }
   if (p->couple_smem > (size_t)prop.sharedMemPerBlockOptin)
     throw Status{SLSHT_ERR_VALIDATION, "window band limit too large for the shared-memory tile"};
-  CK(cudaFuncSetAttribute(couple_kernel(p->n, p->MG, p->NG),
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->couple_smem));
   CK(cudaStreamSynchronize(s));
 }
 
@@ -469,8 +560,10 @@ void run_setup(slsht_cuda_plan* p) {
   const int wmax = (2 * L + 1) * (2 * L + 1) * p->nb;
   k_dtab<<<dim3((wmax + 255) / 256, L + 1), 256, 0, s>>>(L, p->d_delta, p->d_rou, p->d_dtab);
   CKL();
-  k_wtab<<<dim3((p->ncol + 127) / 128, p->NPQ), 128, 0, s>>>(L, p->d_h, p->d_dtab, p->d_rou,
-                                                             p->d_pq, p->d_W);
+  const int tile_nt = p->use_ws ? p->ws.NT : 0;
+  const int ncol_pad = p->use_ws ? p->n_col_tiles * p->ws.NT : p->ncol;
+  k_wtab<<<dim3((ncol_pad + 127) / 128, p->NPQ), 128, 0, s>>>(L, p->d_h, p->d_dtab, p->d_rou,
+                                                             p->d_pq, tile_nt, ncol_pad, p->d_W);
   CKL();
   p->launches += 6;
   record(p, 1);
@@ -487,7 +580,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   record(p, 1);
   k_modgemm<<<dim3(ch.ntile, (p->NPQ + MG_COLS - 1) / MG_COLS), 256, 0, s>>>(
       p->d_tiles + ch.tile0, p->n_nodes, p->ldA, p->L_f, p->NPQ, p->d_A, p->d_itab, p->d_lamh,
-      p->d_pq, p->d_U);
+      p->d_pq, p->use_ws ? p->ws.MT : 0, p->ws_stages.group_elems, p->d_ubase, p->d_ustr, p->d_U);
   CKL();
   record(p, 2);
   CoupleParams prm{};
@@ -513,8 +606,20 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   prm.fft = p->fft;
   prm.generic_dft = p->generic_dft;
   const int MT = 8 * p->MG;
-  dim3 grid(p->n_col_tiles, (ch.count + MT - 1) / MT);
-  couple_kernel(p->n, p->MG, p->NG)<<<grid, couple_threads(p->n), p->couple_smem, s>>>(prm);
+  if (p->use_ws) {
+    WsParams wp{};
+    wp.c = prm;
+    wp.st = p->ws_stages;
+    wp.n_groups = (ch.count + MT - 1) / MT;
+    wp.n_tiles = wp.n_groups * p->n_col_tiles;
+    wp.ct_fast = p->ct_fast;
+    int grid = std::min(wp.n_tiles, p->num_sms);
+    if (const char* g = std::getenv("SLSHT_CUDA_WS_GRID")) grid = std::max(1, std::min(grid, std::atoi(g)));
+    p->ws.fn<<<grid, p->ws.threads, p->couple_smem, s>>>(wp);
+  } else {
+    dim3 grid(p->n_col_tiles, (ch.count + MT - 1) / MT);
+    couple_kernel(p->n, p->MG, p->NG)<<<grid, couple_threads(p->n), p->couple_smem, s>>>(prm);
+  }
   CKL();
   record(p, 3);
   k_digest<<<(ch.count + 3) / 4, 128, 0, s>>>(comps, ch.count, p->n_col_tiles, p->n,
@@ -816,7 +921,8 @@ int slsht_cuda_modulated(slsht_cuda_plan* p, const double* f, int count, const i
         ds, p->L_g, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_weights, A);
     CKL();
     k_modgemm<<<dim3(count, (p->NPQ + MG_COLS - 1) / MG_COLS), 256, 0, s>>>(
-        dt, p->n_nodes, p->ldA, p->L_f, p->NPQ, A, p->d_itab, p->d_lamh, p->d_pq, U);
+        dt, p->n_nodes, p->ldA, p->L_f, p->NPQ, A, p->d_itab, p->d_lamh, p->d_pq, 0, 0, nullptr,
+        nullptr, U);
     CKL();
     std::vector<double2> hU((size_t)count * p->NPQ);
     CK(cudaMemcpyAsync(hU.data(), U, hU.size() * 16, cudaMemcpyDeviceToHost, s));
