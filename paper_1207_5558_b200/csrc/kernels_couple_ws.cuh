@@ -65,11 +65,13 @@ struct WsStages {
   int js[136];    // n + 1 entries at most (n <= 129 for the compile-time lengths)
   int uoff[136];
   int ustr[136];
+  int urb[136];           // per q row jq: offset of its zero-padded row block in its U stage
   long long group_elems;  // U elements per component group
 };
 
 struct WsParams {
   CoupleParams c;
+  long long* trace;  // debug: per-tile phase timestamps of CTA 0 (SLSHT_WS_TRACE builds)
   WsStages st;
   int n_groups;  // component groups of MT in this chunk
   int n_tiles;   // n_groups * n_col_tiles
@@ -87,7 +89,7 @@ struct WsCfg {
   static constexpr int USTR = RS + 8;                // max 16-B units per staged U row
   static constexpr size_t T_BYTES = (size_t)MT * N * NT * 16;
   static constexpr size_t U_BYTES = (size_t)MT * USTR * 16;
-  static constexpr size_t W_BYTES = (size_t)RS * NT * 16;
+  static constexpr size_t W_BYTES = (size_t)(RS + 4) * NT * 16;  // +4 spare rows read by partial k-steps
   static constexpr size_t STAGE_BYTES = U_BYTES + W_BYTES;
   static constexpr size_t OFF_STAGE = 2 * T_BYTES;
   static constexpr size_t OFF_TAB = OFF_STAGE + NSTAGE * STAGE_BYTES;
@@ -98,6 +100,76 @@ struct WsCfg {
   static_assert(T_BYTES >= (size_t)GT * 8 * 8, "T buffer doubles as reduction scratch");
   static_assert(RS % 4 == 0, "stage rows in k-steps");
 };
+
+// Output rows a = A0, A0 + A_STEP, ... of one (component, column) transform: the permutation is
+// a compile-time table, so every T read is a constant offset.
+template <int N>
+struct DifPerm {
+  int v[N];
+  constexpr DifPerm() : v() {
+    int fac[16] = {}, nf = 0, x = N;
+    for (int p = 3; x > 1; p += 2)
+      while (x % p == 0) {
+        fac[nf++] = p;
+        x /= p;
+      }
+    for (int pos = 0; pos < N; ++pos) {
+      int rem = pos, freq = 0, mult = 1, mm = N;
+      for (int i = 0; i < nf; ++i) {
+        const int mp = mm / fac[i], k = rem / mp;
+        rem %= mp;
+        freq += k * mult;
+        mult *= fac[i];
+        mm = mp;
+      }
+      v[freq] = pos;
+    }
+  }
+};
+
+template <int N, int NT, int PAIRS, int A_STEP, int A0>
+__device__ __forceinline__ void ws_epilogue(const double2* T, const int* perm_s,
+                                            const CoupleParams& P, const CompRec& rec, int cl,
+                                            int cc, int col, double& s2, long long& mx2,
+                                            double& pr, double& pi, double& ir, double& ii,
+                                            double& g0r, double& g0i) {
+  constexpr DifPerm<N> kPerm{};
+  (void)perm_s;
+  double2* o = P.out + rec.slot * P.vol + col + (size_t)A0 * P.ncol;
+  double2* om = (P.mirror && rec.m > 0) ? P.out + rec.mslot * P.vol + col + (size_t)A0 * P.ncol
+                                        : nullptr;
+  const long long sbit = (long long)0x8000000000000000ULL;
+  const long long fr = (rec.m & 1) ? sbit : 0, fi = (rec.m & 1) ? 0 : sbit;
+  const double2* Tp = T + (size_t)cl * N * NT + cc;
+  const size_t ostep = (size_t)A_STEP * P.ncol;
+  uint32_t hsh = (uint32_t)((size_t)A0 * P.ncol + col) * 0x9E3779B1u;
+  const uint32_t hstep = (uint32_t)ostep * 0x9E3779B1u;
+  if (A0 == 0 && col == 0) {
+    const double2 v = Tp[kPerm.v[0] * NT];
+    g0r = v.x;
+    g0i = v.y;
+  }
+#pragma unroll
+  for (int a = A0; a < N; a += A_STEP) {
+    const double2 v = Tp[kPerm.v[a] * NT];
+    *o = v;
+    o += ostep;
+    if (om) {
+      *om = make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ fr),
+                         __longlong_as_double(__double_as_longlong(v.y) ^ fi));
+      om += ostep;
+    }
+    const double a2 = fma(v.x, v.x, v.y * v.y);
+    s2 += a2;
+    mx2 = max(mx2, __double_as_longlong(a2));
+    const double wgt = digest_weight(hsh);
+    hsh += hstep;
+    pr = fma(wgt, v.x, pr);
+    pi = fma(wgt, v.y, pi);
+    ir += v.x;
+    ii += v.y;
+  }
+}
 
 // Ping-pong persistent kernel: a producer warp streams the operand stages of the CTA's tiles in
 // order through the ring; consumer group k (GW warps) owns every other tile and its own T
@@ -129,6 +201,13 @@ __global__ void __launch_bounds__(WsCfg<N, MG, NG, RS, NSTAGE, GW>::NTHREADS, 1)
   }
   for (int i = tid; i <= N; i += Cfg::NTHREADS) qoff_s[i] = P.qoff[i];
   for (int i = tid; i <= L; i += Cfg::NTHREADS) betaw_s[i] = P.betaw[i];
+  {
+    // W rows past a stage's rows are read (times a zero U pad) by partial k-steps: keep the
+    // ring finite from the start
+    double4* ring = reinterpret_cast<double4*>(smem + Cfg::OFF_STAGE);
+    for (size_t i = tid; i < NSTAGE * Cfg::STAGE_BYTES / 32; i += Cfg::NTHREADS)
+      ring[i] = make_double4(0.0, 0.0, 0.0, 0.0);
+  }
   if (tid == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full[s], 1);
@@ -198,10 +277,32 @@ __global__ void __launch_bounds__(WsCfg<N, MG, NG, RS, NSTAGE, GW>::NTHREADS, 1)
     int g, ct;
     tile_of(t, g, ct);
     const int comp0 = g * MT, col0 = ct * NT;
+    constexpr int A_STEP = GT / PAIRS;
+    const int pair = gt % PAIRS;
+    const int cl = pair / NT, cc = pair % NT;
+    const int a_first = gt / PAIRS;  // warp-uniform
+    const int comp = comp0 + cl, col = col0 + cc;
+    const bool ok = comp < P.count && col < P.ncol;
+    CompRec rec{0, 0, 0, -1};
+    if (ok) rec = P.comps[comp];  // in flight during the MMA phase
     // ---------------- MMA phase: items (q, warp tile), q-major, one per warp per round
+#ifdef SLSHT_WS_TRACE
+    const bool tr = WP.trace && blockIdx.x == 0 && gt == 0 && k_local < 64;
+    if (tr) WP.trace[k_local * 6 + 0] = clock64();
+#endif
     if (k_local > 0) mbar_wait(turn, (uint32_t)((k_local - 1) & 1));
+#ifdef SLSHT_WS_TRACE
+    if (tr) WP.trace[k_local * 6 + 1] = clock64();
+#endif
     for (int s = 0; s < nst; ++s) {
+#ifdef SLSHT_WS_TRACE
+      long long tw0 = clock64();
+#endif
       mbar_wait(&full[stage], phase);
+#ifdef SLSHT_WS_TRACE
+      if (tr && s < 8) WP.trace[384 + k_local * 16 + 2 * s] = clock64() - tw0;
+      tw0 = clock64();
+#endif
       const double2* Us =
           reinterpret_cast<const double2*>(smem + Cfg::OFF_STAGE + stage * Cfg::STAGE_BYTES);
       const double2* Ws = Us + MT * USTR;
@@ -209,93 +310,71 @@ __global__ void __launch_bounds__(WsCfg<N, MG, NG, RS, NSTAGE, GW>::NTHREADS, 1)
       const int r0 = qoff_s[j0];
       const int ustr = WP.st.ustr[s];
       const int n_items = (j1 - j0) * WT;
+#ifdef SLSHT_WS_NO_MMA
+      if (false)
+#endif
       for (int it = gw; it < n_items; it += GW) {
         const int jq = j0 + it / WT, wt = it % WT;
         const int np = L + 1 - abs(jq - L);
-        const int rb = qoff_s[jq] - r0;
+        const int nks = (np + 3) >> 2;
+        const int wrb = qoff_s[jq] - r0;  // W rows of q in the stage
         const int ar = (wt / NG) * 8 + (lane >> 2);
-        const int bc = (wt % NG) * 8 + (lane >> 2);
-        const int bsw_hi = bc & ~7, bsw_lo = bc & 7;
-        // branch-free fragments: rows clamped into the q's range, A zeroed past np (B x 0 = 0)
-        auto frag = [&](int ks, double& s_, double& ax, double& ay, double& bx, double& d_, double& e_) {
-          const int k = 4 * ks + kl;
-          const int r = rb + min(k, np - 1);
-          const double2 a = Us[ar * ustr + r];
-          const double2 b = Ws[r * NT + (bsw_hi | (bsw_lo ^ ((2 * (r0 + r)) & 7)))];
-          const bool keep = k < np;
-          ax = keep ? a.x : 0.0;
-          ay = keep ? a.y : 0.0;
-          s_ = ax + ay;
-          bx = b.x;
-          d_ = b.y - b.x;
-          e_ = b.x + b.y;
-        };
+        const int bhi = (wt % NG) * 8, blo = lane >> 2;
+        // U rows of q are zero-padded to whole k-steps, so no masking; the W swizzle of a lane
+        // is the same in every k-step (rows advance by 4, 2*4 == 0 mod 8)
+        const double2* ap = Us + ar * ustr + WP.st.urb[jq] + kl;
+        const double2* bp = Ws + (wrb + kl) * NT + (bhi | (blo ^ ((2 * (r0 + wrb + kl)) & 7)));
         double c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0}, c3[2] = {0.0, 0.0};
-        const int ks_n = (np + 3) / 4;
-        double s_, ax, ay, bx, d_, e_;
-        frag(0, s_, ax, ay, bx, d_, e_);
-        for (int ks = 0; ks < ks_n; ++ks) {
-          double ns_, nax, nay, nbx, nd_, ne_;
-          frag(min(ks + 1, ks_n - 1), ns_, nax, nay, nbx, nd_, ne_);
-          dmma(c1[0], c1[1], s_, bx);
-          dmma(c2[0], c2[1], ax, d_);
-          dmma(c3[0], c3[1], ay, e_);
-          s_ = ns_; ax = nax; ay = nay; bx = nbx; d_ = nd_; e_ = ne_;
+        double2 a = ap[0], b = bp[0];
+        for (int ks = 0; ks < nks; ++ks) {
+          const int kn = min(ks + 1, nks - 1);
+          const double2 na = ap[4 * kn], nb = bp[4 * kn * NT];
+          dmma(c1[0], c1[1], a.x + a.y, b.x);
+          dmma(c2[0], c2[1], a.x, b.y - b.x);
+          dmma(c3[0], c3[1], a.y, b.x + b.y);
+          a = na;
+          b = nb;
         }
         const int row = jq >= L ? jq - L : jq + L + 1;  // q mod n
-        double2* dst = T + (size_t)(ar * N + row) * NT + bsw_hi + 2 * kl;
+        double2* dst = T + (size_t)(ar * N + row) * NT + bhi + 2 * kl;
         dst[0] = make_double2(c1[0] - c3[0], c1[0] + c2[0]);
         dst[1] = make_double2(c1[1] - c3[1], c1[1] + c2[1]);
       }
       __syncwarp();
+#ifdef SLSHT_WS_TRACE
+      if (tr && s < 8) WP.trace[384 + k_local * 16 + 2 * s + 1] = clock64() - tw0;
+#endif
       if (lane == 0) mbar_arrive(&empty[stage]);
       advance(1);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(turn);
+#ifdef SLSHT_WS_TRACE
+    if (tr) WP.trace[k_local * 6 + 2] = clock64();
+#endif
     named_sync(bar_id, GT);
+#ifdef SLSHT_WS_TRACE
+    if (tr) WP.trace[k_local * 6 + 3] = clock64();
+#endif
+#ifdef SLSHT_WS_NO_EPI
+    continue;
+#endif
     // ---------------- alpha FFT in place
     FftDif<N, N, NT, PAIRS, GT>::run(T, rou_s, gt, bar_id);
     // ---------------- epilogue: stores, mirror, digest partials
-    const int pair = gt % PAIRS;
-    const int cl = pair / NT, cc = pair % NT;
-    constexpr int A_STEP = GT / PAIRS;
-    const int comp = comp0 + cl, col = col0 + cc;
-    const bool ok = comp < P.count && col < P.ncol;
+#ifdef SLSHT_WS_TRACE
+    if (tr) WP.trace[k_local * 6 + 4] = clock64();
+#endif
     double s2 = 0.0, pr = 0.0, pi = 0.0, ir = 0.0, ii = 0.0, g0r = 0.0, g0i = 0.0;
     long long mx2 = 0;
     if (ok) {
-      const CompRec rec = P.comps[comp];
-      double2* o = P.out + rec.slot * P.vol + col;
-      double2* om = (P.mirror && rec.m > 0) ? P.out + rec.mslot * P.vol + col : nullptr;
-      const long long sbit = (long long)0x8000000000000000ULL;
-      const long long fr = (rec.m & 1) ? sbit : 0, fi = (rec.m & 1) ? 0 : sbit;
+      if (a_first == 0)
+        ws_epilogue<N, NT, PAIRS, A_STEP, 0>(T, perm_s, P, rec, cl, cc, col, s2, mx2, pr, pi, ir, ii,
+                                             g0r, g0i);
+      else if constexpr (A_STEP > 1)
+        ws_epilogue<N, NT, PAIRS, A_STEP, 1>(T, perm_s, P, rec, cl, cc, col, s2, mx2, pr, pi, ir, ii,
+                                             g0r, g0i);
       const double qb = betaw_s[col / N];
-      const double2* Tp = T + (size_t)cl * N * NT + cc;
-      const int a_first = gt / PAIRS;
-      uint32_t hsh = (uint32_t)((size_t)a_first * P.ncol + col) * 0x9E3779B1u;
-      const uint32_t hstep = (uint32_t)((size_t)A_STEP * P.ncol) * 0x9E3779B1u;
-#pragma unroll 4
-      for (int a = a_first; a < N; a += A_STEP, hsh += hstep) {
-        const double2 v = Tp[(size_t)perm_s[a] * NT];
-        const size_t idx = (size_t)a * P.ncol;
-        o[idx] = v;
-        if (om)
-          om[idx] = make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ fr),
-                                 __longlong_as_double(__double_as_longlong(v.y) ^ fi));
-        const double a2 = fma(v.x, v.x, v.y * v.y);
-        s2 += a2;
-        mx2 = max(mx2, __double_as_longlong(a2));
-        const double wgt = digest_weight(hsh);
-        pr = fma(wgt, v.x, pr);
-        pi = fma(wgt, v.y, pi);
-        ir += v.x;
-        ii += v.y;
-        if (a == 0 && col == 0) {
-          g0r = v.x;
-          g0i = v.y;
-        }
-      }
       ir *= qb;
       ii *= qb;
     }
@@ -323,6 +402,9 @@ __global__ void __launch_bounds__(WsCfg<N, MG, NG, RS, NSTAGE, GW>::NTHREADS, 1)
       }
     }
     named_sync(bar_id, GT);  // scratch read before the next tile's MMA writes T
+#ifdef SLSHT_WS_TRACE
+    if (tr) WP.trace[k_local * 6 + 5] = clock64();
+#endif
   }
 }
 

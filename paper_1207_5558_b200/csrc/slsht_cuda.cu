@@ -14,6 +14,7 @@
 #include "kernels_chunk.cuh"
 #include "kernels_couple.cuh"
 #include "kernels_couple_ws.cuh"
+#include "kernels_couple_lines.cuh"
 #include "kernels_setup.cuh"
 #include "slsht_cuda.h"
 
@@ -100,6 +101,11 @@ struct slsht_cuda_plan {
   WsKernel ws{};
   WsStages ws_stages{};
   int num_sms = 0;
+  bool use_lines = false;  // line-aligned persistent coupling kernel (n <= 33, ncol % 8 == 1)
+  void (*lines_fn)(LnParams) = nullptr;
+  int lines_threads = 0;
+  int lines_upad = 0;
+  int lines_urb[136] = {};
   int* d_ubase = nullptr;  // stage-tiled U layout (ws path): per (p, q) row block offset
   int* d_ustr = nullptr;   //   and row stride
   int ct_fast = 0;
@@ -287,7 +293,23 @@ void build_plan(slsht_cuda_plan* p) {
   p->ldA = (p->n_nodes + MG_K - 1) / MG_K * MG_K;
   p->vol = (long long)p->n * p->n * p->nb;
   couple_tile(p->n, p->MG, p->NG);
-  if (std::getenv("SLSHT_CUDA_NO_WS") == nullptr && ws_kernel(p->n, p->ws)) {
+  if (std::getenv("SLSHT_CUDA_LINES") != nullptr && (p->ncol % 8) == 1 &&
+      (p->n == 17 || p->n == 33)) {
+    p->use_lines = true;
+    p->MG = 1;
+    p->NG = 1;
+    if (p->n == 17) {
+      p->lines_fn = k_couple_lines<17, 16>;
+      p->lines_threads = LnCfg<17, 16>::NTHREADS;
+      p->couple_smem = LnCfg<17, 16>::SMEM;
+      p->lines_upad = LnCfg<17, 16>::UPAD;
+    } else {
+      p->lines_fn = k_couple_lines<33, 16>;
+      p->lines_threads = LnCfg<33, 16>::NTHREADS;
+      p->couple_smem = LnCfg<33, 16>::SMEM;
+      p->lines_upad = LnCfg<33, 16>::UPAD;
+    }
+  } else if (std::getenv("SLSHT_CUDA_NO_WS") == nullptr && ws_kernel(p->n, p->ws)) {
     p->use_ws = true;
     p->MG = p->ws.MT / 8;
     p->NG = p->ws.NT / 8;
@@ -295,7 +317,7 @@ void build_plan(slsht_cuda_plan* p) {
     int cnt = 0, rows = 0;
     p->ws_stages.js[0] = 0;
     for (int jq = 0; jq < p->n; ++jq) {
-      const int np = L + 1 - std::abs(jq - L);
+      const int np = (L + 1 - std::abs(jq - L) + 3) / 4 * 4;  // padded to whole k-steps
       if (rows + np > p->ws.RS) {
         p->ws_stages.js[++cnt] = jq;
         rows = 0;
@@ -345,18 +367,41 @@ void build_plan(slsht_cuda_plan* p) {
     const int MT = p->ws.MT;
     long long off = 0;
     for (int st = 0; st < p->ws_stages.count; ++st) {
-      const int r0 = qoff[p->ws_stages.js[st]], r1 = qoff[p->ws_stages.js[st + 1]];
-      const int rows = r1 - r0;
-      const int us = rows + (((4 - rows) % 8) + 8) % 8;
+      // each q's rows padded with zeros to whole k-steps of 4 (the MMA loop never masks)
+      int rows_pad = 0;
+      for (int jq = p->ws_stages.js[st]; jq < p->ws_stages.js[st + 1]; ++jq) {
+        p->ws_stages.urb[jq] = rows_pad;
+        rows_pad += (qoff[jq + 1] - qoff[jq] + 3) / 4 * 4;
+      }
+      const int us = rows_pad + (((4 - rows_pad) % 8) + 8) % 8;  // == 4 mod 8: no bank conflicts
+      if (us + 8 > p->ws.RS + 8 + 8)
+        throw Status{SLSHT_ERR_VALIDATION, "internal: operand stage exceeds its buffer"};
       p->ws_stages.uoff[st] = (int)off;
       p->ws_stages.ustr[st] = us;
-      for (int c = r0; c < r1; ++c) {
-        ubase[c] = (int)off + (c - r0);
-        ustr[c] = us;
-      }
+      for (int jq = p->ws_stages.js[st]; jq < p->ws_stages.js[st + 1]; ++jq)
+        for (int c = qoff[jq]; c < qoff[jq + 1]; ++c) {
+          ubase[c] = (int)off + p->ws_stages.urb[jq] + (c - qoff[jq]);
+          ustr[c] = us;
+        }
       off += (long long)MT * us;
     }
     p->ws_stages.group_elems = off;
+  }
+  if (p->use_lines) {
+    // one padded block per component: q rows padded with zeros to whole k-steps of 4
+    int rows_pad = 0;
+    for (int jq = 0; jq < p->n; ++jq) {
+      p->lines_urb[jq] = rows_pad;
+      rows_pad += (qoff[jq + 1] - qoff[jq] + 3) / 4 * 4;
+    }
+    if (rows_pad > p->lines_upad)
+      throw Status{SLSHT_ERR_VALIDATION, "internal: padded U rows exceed the line kernel buffer"};
+    for (int jq = 0; jq < p->n; ++jq)
+      for (int c = qoff[jq]; c < qoff[jq + 1]; ++c) {
+        ubase[c] = p->lines_urb[jq] + (c - qoff[jq]);
+        ustr[c] = p->lines_upad;
+      }
+    p->ws_stages.group_elems = 8LL * p->lines_upad;
   }
   // ---- alpha-axis FFT plan: roots of unity, DIF stages, output permutation, phase shift
   const int n = p->n;
@@ -474,7 +519,8 @@ void build_plan(slsht_cuda_plan* p) {
   for (int pp = 0; pp <= L; ++pp) dsz += (size_t)(2 * pp + 1) * (2 * pp + 1);
   p->d_delta = dalloc<double>(dsz);
   p->d_dtab = dalloc<double>(dsz * p->nb);
-  const size_t ncol_pad = p->use_ws ? (size_t)p->n_col_tiles * p->ws.NT : (size_t)p->ncol;
+  const int tile_nt_alloc = p->use_lines ? 8 : (p->use_ws ? p->ws.NT : 0);
+  const size_t ncol_pad = tile_nt_alloc ? (size_t)p->n_col_tiles * tile_nt_alloc : (size_t)p->ncol;
   p->d_W = dalloc<double2>((size_t)p->NPQ * ncol_pad);
   p->ct_fast = (size_t)p->NPQ * ncol_pad * 16 < (48u << 20);
   p->d_ubase = dupload(ubase, s);
@@ -490,9 +536,11 @@ void build_plan(slsht_cuda_plan* p) {
   p->d_segs = dupload(p->segs, s);
   p->d_tiles = dupload(p->tiles, s);
   p->d_A = dalloc<double>((size_t)p->max_chunk * p->ldA);
-  if (p->use_ws) {
-    const size_t groups = (size_t)(p->max_chunk + p->ws.MT - 1) / p->ws.MT;
+  if (p->use_ws || p->use_lines) {
+    const int gmt = p->use_lines ? 8 : p->ws.MT;
+    const size_t groups = (size_t)(p->max_chunk + gmt - 1) / gmt;
     p->d_U = dalloc<double2>(groups * (size_t)p->ws_stages.group_elems);
+    CK(cudaMemsetAsync(p->d_U, 0, groups * (size_t)p->ws_stages.group_elems * 16, s));
   } else {
     p->d_U = dalloc<double2>((size_t)p->max_chunk * p->NPQ);
   }
@@ -513,7 +561,10 @@ void build_plan(slsht_cuda_plan* p) {
   for (auto& e : p->ev_stage) CK(cudaEventCreate(&e));
 
   p->num_sms = prop.multiProcessorCount;
-  if (p->use_ws) {
+  if (p->use_lines) {
+    CK(cudaFuncSetAttribute(p->lines_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)p->couple_smem));
+  } else if (p->use_ws) {
     p->couple_smem = p->ws.smem;
     CK(cudaFuncSetAttribute(p->ws.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)p->couple_smem));
@@ -560,8 +611,8 @@ void run_setup(slsht_cuda_plan* p) {
   const int wmax = (2 * L + 1) * (2 * L + 1) * p->nb;
   k_dtab<<<dim3((wmax + 255) / 256, L + 1), 256, 0, s>>>(L, p->d_delta, p->d_rou, p->d_dtab);
   CKL();
-  const int tile_nt = p->use_ws ? p->ws.NT : 0;
-  const int ncol_pad = p->use_ws ? p->n_col_tiles * p->ws.NT : p->ncol;
+  const int tile_nt = p->use_lines ? 8 : (p->use_ws ? p->ws.NT : 0);
+  const int ncol_pad = tile_nt ? p->n_col_tiles * tile_nt : p->ncol;
   k_wtab<<<dim3((ncol_pad + 127) / 128, p->NPQ), 128, 0, s>>>(L, p->d_h, p->d_dtab, p->d_rou,
                                                              p->d_pq, tile_nt, ncol_pad, p->d_W);
   CKL();
@@ -580,7 +631,8 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   record(p, 1);
   k_modgemm<<<dim3(ch.ntile, (p->NPQ + MG_COLS - 1) / MG_COLS), 256, 0, s>>>(
       p->d_tiles + ch.tile0, p->n_nodes, p->ldA, p->L_f, p->NPQ, p->d_A, p->d_itab, p->d_lamh,
-      p->d_pq, p->use_ws ? p->ws.MT : 0, p->ws_stages.group_elems, p->d_ubase, p->d_ustr, p->d_U);
+      p->d_pq, p->use_lines ? 8 : (p->use_ws ? p->ws.MT : 0), p->ws_stages.group_elems,
+      p->d_ubase, p->d_ustr, p->d_U);
   CKL();
   record(p, 2);
   CoupleParams prm{};
@@ -606,27 +658,81 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   prm.fft = p->fft;
   prm.generic_dft = p->generic_dft;
   const int MT = 8 * p->MG;
-  if (p->use_ws) {
+  if (p->use_lines) {
+    LnParams lp{};
+    lp.c = prm;
+    lp.group_elems = p->ws_stages.group_elems;
+    for (int i = 0; i < p->n; ++i) lp.urb[i] = p->lines_urb[i];
+    lp.n_groups = (ch.count + 7) / 8;
+    lp.digest = p->d_digest;
+    lp.trace = nullptr;
+    const int grid = std::min(lp.n_groups, p->num_sms);
+#ifdef SLSHT_WS_TRACE
+    static long long* d_ltrace = nullptr;
+    if (!d_ltrace) CK(cudaMalloc(&d_ltrace, 2048 * sizeof(long long)));
+    CK(cudaMemsetAsync(d_ltrace, 0, 2048 * sizeof(long long), s));
+    lp.trace = d_ltrace;
+#endif
+    p->lines_fn<<<grid, p->lines_threads, p->couple_smem, s>>>(lp);
+#ifdef SLSHT_WS_TRACE
+    {
+      long long h[64 * 6];
+      CK(cudaMemcpyAsync(h, d_ltrace, sizeof(h), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int k = 0; k < 8; ++k)
+        fprintf(stderr, "lines tile %2d: start %8lld wwait %6lld mma %6lld fft %6lld digest %6lld lines %6lld\n",
+                k, h[6 * k] - h[0], h[6 * k + 1] - h[6 * k], h[6 * k + 2] - h[6 * k + 1],
+                h[6 * k + 3] - h[6 * k + 2], h[6 * k + 4] - h[6 * k + 3], h[6 * k + 5] - h[6 * k + 4]);
+    }
+#endif
+  } else if (p->use_ws) {
     WsParams wp{};
     wp.c = prm;
     wp.st = p->ws_stages;
     wp.n_groups = (ch.count + MT - 1) / MT;
     wp.n_tiles = wp.n_groups * p->n_col_tiles;
     wp.ct_fast = p->ct_fast;
+    wp.trace = nullptr;
+#ifdef SLSHT_WS_TRACE
+    static long long* d_trace = nullptr;
+    if (!d_trace) CK(cudaMalloc(&d_trace, 2048 * sizeof(long long)));
+    CK(cudaMemsetAsync(d_trace, 0, 2048 * sizeof(long long), s));
+    wp.trace = d_trace;
+#endif
     int grid = std::min(wp.n_tiles, p->num_sms);
     if (const char* g = std::getenv("SLSHT_CUDA_WS_GRID")) grid = std::max(1, std::min(grid, std::atoi(g)));
     p->ws.fn<<<grid, p->ws.threads, p->couple_smem, s>>>(wp);
+#ifdef SLSHT_WS_TRACE
+    {
+      long long h[2048];
+      CK(cudaMemcpyAsync(h, d_trace, sizeof(h), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      const long long t0 = h[0];
+      for (int k = 0; k < 12; ++k)
+        fprintf(stderr, "tile %2d grp %d: start %8lld turn %6lld mma %6lld sync %6lld fft %6lld epi %6lld\n",
+                k, k & 1, h[6 * k] - t0, h[6 * k + 1] - h[6 * k], h[6 * k + 2] - h[6 * k + 1],
+                h[6 * k + 3] - h[6 * k + 2], h[6 * k + 4] - h[6 * k + 3], h[6 * k + 5] - h[6 * k + 4]);
+      for (int k = 0; k < 6; ++k) {
+        fprintf(stderr, "  tile %d stages (wait/compute):", k);
+        for (int st = 0; st < 8; ++st)
+          fprintf(stderr, " %lld/%lld", h[384 + k * 16 + 2 * st], h[384 + k * 16 + 2 * st + 1]);
+        fprintf(stderr, "\n");
+      }
+    }
+#endif
   } else {
     dim3 grid(p->n_col_tiles, (ch.count + MT - 1) / MT);
     couple_kernel(p->n, p->MG, p->NG)<<<grid, couple_threads(p->n), p->couple_smem, s>>>(prm);
   }
   CKL();
   record(p, 3);
-  k_digest<<<(ch.count + 3) / 4, 128, 0, s>>>(comps, ch.count, p->n_col_tiles, p->n,
-                                                  p->d_partials, p->mirror, p->d_digest);
-  CKL();
+  if (!p->use_lines) {  // the line kernel writes the digests itself
+    k_digest<<<(ch.count + 3) / 4, 128, 0, s>>>(comps, ch.count, p->n_col_tiles, p->n,
+                                                    p->d_partials, p->mirror, p->d_digest);
+    CKL();
+  }
   record(p, 4);
-  p->launches += 4;
+  p->launches += p->use_lines ? 3 : 4;
   if (p->profile) {
     accumulate(p, ST_LEGENDRE, 0, 1);
     accumulate(p, ST_MODGEMM, 1, 2);
