@@ -246,6 +246,20 @@ def run_ours(args) -> None:
     total_samples = cfg.samples()
     value = total_samples / (ms_per_step / 1e3)
 
+    # ---- the one collective (N > 1): digest rows of every degree shard gathered on rank 0
+    gather = None
+    if world > 1:
+        from paper_1207_5558_b200.parallel import gather_digests
+
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record()
+        full = gather_digests(dig_dev, l0, l1, cfg.L_g)
+        g1.record()
+        torch.cuda.synchronize(dev)
+        gather = {"ms": g0.elapsed_time(g1), "rows": int((cfg.L_g + 1) ** 2),
+                  "complete": bool(rank != 0 or not torch.isnan(full).any().item())}
+
     # ---- e2e: C ABI with host buffers (pinned), H2D of f, h and D2H of digests inside
     f_pin = torch.from_numpy(f_np.view(np.float64).copy()).pin_memory()
     h_pin = torch.from_numpy(h_np.view(np.float64).copy()).pin_memory()
@@ -355,6 +369,7 @@ def run_ours(args) -> None:
             "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
+            "gather": gather,
             "gpu_launches": launches_per_step * args.steps,
             "gpu_launches_per_step": launches_per_step,
         }
