@@ -1,23 +1,28 @@
-// Line-aligned persistent coupling kernel for the small transform lengths (n <= 33), where the
-// output stream dominates ("store path").
+// Line-aligned persistent coupling kernel for the small transform lengths (n = 17, 33), where
+// the output stream dominates ("store path").
 //
 // Why: every BASELINE volume row holds ncol = n (L_h+1) complex, an odd count, so the rows of an
-// So3Volume start at alternating (and generally unaligned) 16-B offsets. A kernel that stores
-// column strips writes every row as a misaligned 128-B segment, i.e. two partial L2 lines, and
-// the B200 write path then saturates at ~2.3 TB/s whatever the store instruction (STG, TMA
-// tensor store, cache policy: profiles/store_microbench.txt). Full aligned lines reach 4.3+.
+// So3Volume start at unaligned 16-B offsets. A kernel that stores column strips writes every
+// row as a misaligned 128-B segment, i.e. two partial L2 lines, and the B200 write path then
+// saturates at ~2.3 TB/s whatever the store instruction (STG, TMA tensor store, cache policy:
+// profiles/microbench_store_*.txt). Whole aligned 128-B lines reach 4.3+ TB/s.
 //
 // How: a CTA owns one group of MT = 8 components at a time and walks its column tiles
-// ct = 0, 1, ... in order. U of the group stays resident in shared memory (one bulk copy);
-// the W column tile streams through a 2-deep ring (one bulk copy per tile). After the DMMA
-// coupling and the in-place alpha FFT of tile ct, the epilogue writes, for every
-// (component, row a), exactly the one 128-B line whose last element falls inside the tile's
-// columns of that row; the first part of that line comes from tile ct-1 (still resident in
-// the other T buffer). Lines that cross a row boundary are written when the last tile of the
-// row is done, from a kept copy of tile 0. Only the two lines at each volume's ends can be
-// partial. The mirror volume (real mode) has its own line phase and is written the same way.
-// The digest of each component accumulates over its tiles in registers (one warp per
-// component, fixed order) and is written once per group, so no partials pass is needed.
+// ct = 0, 1, ... in order (8 columns each).
+//   producer warp : the group's U block (resident for the whole group, one bulk copy) and the
+//                   whole W column tile through two slots (mbarriers);
+//   compute warps : one warp per first-stage DIF butterfly row group (n = R1 * MP: rows
+//                   r + k MP, k < R1). The warp runs the R1 DMMA chains of its rows (Gauss
+//                   3-product complex MMA), applies the radix-R1 butterfly and twiddles to the
+//                   accumulators in registers and writes T; the remaining DIF stages run in
+//                   shared memory, the last one also accumulating the digest of its outputs;
+//   store warps   : 16 line groups = (component, volume). For every row of the tile the one
+//                   aligned 128-B line that starts in (p0 - 8, p0], p0 = the row's first
+//                   element in the tile, read from the tile's T buffer and the previous tile's
+//                   (3 rolling buffers). The few lines that cross a row end are written as two
+//                   partial lines (tail by the row's last tile, head by the next row's first).
+// Compute runs one tile ahead of the stores (buffer reuse waits for the stores of tile t-2), so
+// the FP64 work overlaps the store stream.
 #pragma once
 
 #include "common.cuh"
@@ -29,38 +34,164 @@ namespace slsht_cuda {
 
 struct LnParams {
   CoupleParams c;
-  long long group_elems;  // U elements per group (stage-tiled layout, zero-padded q blocks)
-  int urb[136];           // per q row jq: offset of its padded row block in the group's U
+  long long group_elems;  // U elements per group: MT rows of UPAD (zero-padded q blocks)
+  int urb[136];           // per q row jq: offset of its padded row block in a U row
   int n_groups;
   double* digest;         // [coeff_count(lmax)][8], rows coeff_index(l, m) (and the mirror)
-  long long* trace;       // debug (SLSHT_WS_TRACE builds): phase timestamps of CTA 0
+  long long* trace;       // debug (SLSHT_WS_TRACE builds)
 };
 
-template <int N, int NWARP>
-struct LnCfg {
+// compile-time q-row layout: rows of q row jq start at qoff(jq); the W halves split at the
+// first jq whose rows start at or past NPQ / 2
+template <int N>
+struct LnRows {
   static constexpr int L = (N - 1) / 2;
   static constexpr int NPQ = (L + 1) * (L + 1);
-  static constexpr int MT = 8, NT = 8;
-  static constexpr int NC = NWARP * 32;            // consumer threads
-  static constexpr int NTHREADS = NC + 32;         // + producer warp
-  static constexpr int UPAD = (NPQ + 3 * N + 8);   // >= padded rows of a group (per component)
-  static constexpr size_t U_BYTES = (size_t)MT * UPAD * 16;
-  static constexpr size_t W_BYTES = (size_t)(NPQ + 8) * NT * 16;
-  static constexpr size_t T_BYTES = (size_t)MT * N * NT * 16;
-  static constexpr size_t OFF_W = U_BYTES;
-  static constexpr size_t OFF_T = OFF_W + 2 * W_BYTES;
-  static constexpr size_t OFF_TAB = OFF_T + 3 * T_BYTES;
-  static constexpr size_t TAB_BYTES =
-      (size_t)N * 16 + (size_t)(L + 1) * 8 + (size_t)(2 * N + 2) * 4 + (size_t)N * 4 + 16 + MT * 24;
-  static constexpr size_t OFF_BAR = (OFF_TAB + TAB_BYTES + 15) / 16 * 16;
-  static constexpr size_t SMEM = OFF_BAR + 6 * 8;
-  static_assert(UPAD % 8 == 4, "U row stride must be 4 mod 8 (16-B units) for conflict-free A loads");
+  static constexpr int np(int jq) { return L + 1 - (jq > L ? jq - L : L - jq); }
+  // U rows of one component: each q row zero-padded to whole k-steps of 4, the total == 4 mod 8
+  // (16-B units) so the 8 component rows of an A fragment hit distinct bank groups
+  static constexpr int urows() {
+    int s = 0;
+    for (int jq = 0; jq < N; ++jq) s += (np(jq) + 3) / 4 * 4;
+    return s;
+  }
+  static constexpr int UPAD = urows() + ((4 - urows()) % 8 + 8) % 8;
 };
 
-template <int N, int NWARP>
-__global__ void __launch_bounds__(LnCfg<N, NWARP>::NTHREADS, 1) k_couple_lines(const LnParams LP) {
-  using Cfg = LnCfg<N, NWARP>;
+template <int N>
+struct LnCfg {
+  using Rows = LnRows<N>;
+  static constexpr int L = (N - 1) / 2;
+  static constexpr int NPQ = Rows::NPQ;
+  static constexpr int MT = 8, NT = 8;
+  static constexpr int R1 = smallest_prime_factor(N);  // first DIF radix: fused into the MMA
+  static constexpr int MP = N / R1;                     // row groups = compute warps
+  static constexpr int NCW = MP;
+  static constexpr int NSW = 4;                         // store warps: 16 (component, volume) lines
+  static constexpr int NC = NCW * 32;
+  static constexpr int NTHREADS = 32 + NC + NSW * 32;
+  static constexpr int UPAD = Rows::UPAD;
+  static constexpr int KSMAX = (L + 1 + 3) / 4;
+  static constexpr size_t U_BYTES = (size_t)MT * UPAD * 16;
+  static constexpr size_t WS_BYTES = (size_t)(NPQ + 4) * NT * 16;  // + rows read by k-step tails
+  static constexpr size_t T_BYTES = (size_t)MT * N * NT * 16;
+  static constexpr size_t OFF_W = U_BYTES;
+  static constexpr size_t OFF_T = OFF_W + 2 * WS_BYTES;
+  static constexpr size_t OFF_TAB = OFF_T + 3 * T_BYTES;
+  static constexpr int RLAST = []() constexpr {  // radix of the last DIF stage
+    int x = N, r = N;
+    for (int p = 3; x > 1; p += 2)
+      while (x % p == 0) {
+        r = p;
+        x /= p;
+      }
+    return r;
+  }();
+  static constexpr int LAST_ITEMS = MT * NT * (N / RLAST);  // butterflies of the last stage
+  static constexpr int NPART = LAST_ITEMS / (MT * NT);       // digest partials per component
+  static constexpr size_t TAB_BYTES = (size_t)N * 16 + (size_t)(L + 1) * 8 + (size_t)(N + 2) * 4 +
+                                      (size_t)N * 4 + 16 + MT * 24 + (size_t)NPART * MT * 8 * 8;
+  static constexpr size_t OFF_BAR = (OFF_TAB + TAB_BYTES + 15) / 16 * 16;
+  static constexpr int NBAR = 2 + 4 + 4;  // ufull uempty | wfull[2] wempty[2] | tready[2] tfree[2]
+  static constexpr size_t SMEM = OFF_BAR + NBAR * 8;
+  static_assert(R1 < N, "the fused first stage needs a composite length");
+  static_assert(LAST_ITEMS <= NC, "one last-stage butterfly per compute thread");
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+// Digest state of one compute thread: its last-stage butterfly always covers the same
+// (component, column-in-tile) pair, so the 8 sums are accumulated in registers across tiles.
+struct DigestAcc {
+  double s2, pr, pi, g0r, g0i, ir, ii;
+  long long mx2;
+};
+
+// Last DIF stage (span R, no twiddles) with the digest of every produced output.
+// Frequency held at position blk * R of the DIF output (R = the last radix): position
+// blk * R + k holds a0 + k (N / R), the last DIF digit being the most significant of the
+// frequency. Thread-constant: computed once, outside the tile loop.
+template <int N, int R>
+__device__ __forceinline__ int dif_last_freq0(int blk) {
+  int a0 = 0, rem = blk * R, mult = 1, mm = N, x = N;
+#pragma unroll
+  for (int p = 3; p <= N; p += 2)
+    if (x > 1)
+      while (x % p == 0) {
+        const int mp = mm / p, d = rem / mp;
+        rem %= mp;
+        a0 += d * mult;
+        mult *= p;
+        mm = mp;
+        x /= p;
+      }
+  return a0;
+}
+
+template <int N, int R, int NT, int PAIRS>
+__device__ __forceinline__ void fft_last_digest(double2* T, int tid, int C, int ncol, int ncomp,
+                                                const double* betaw_s, int a0, DigestAcc& D) {
+  constexpr int TOTAL = PAIRS * (N / R);
+  if (tid >= TOTAL) return;
+  const int pair = tid % PAIRS;
+  const int blk = tid / PAIRS;
+  const int comp = pair / NT, cc = pair % NT;
+  double2* base = T + (size_t)(comp * N + blk * R) * NT + cc;
+  double xr[R], xi[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const double2 v = base[k * NT];
+    xr[k] = v.x;
+    xi[k] = v.y;
+  }
+  Radix<R>::dft(xr, xi);
+#pragma unroll
+  for (int k = 0; k < R; ++k) base[k * NT] = make_double2(xr[k], xi[k]);
+  const int col = C + cc;
+  if (comp >= ncomp || col >= ncol) return;
+  const double qb = betaw_s[col / N];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int a = a0 + k * (N / R);
+    const double vx = xr[k], vy = xi[k];
+    const double a2 = fma(vx, vx, vy * vy);
+    D.s2 += a2;
+    D.mx2 = max(D.mx2, __double_as_longlong(a2));
+    const uint32_t hsh = (uint32_t)((size_t)a * ncol + col) * 0x9E3779B1u;
+    const double wgt = digest_weight(hsh);
+    D.pr = fma(wgt, vx, D.pr);
+    D.pi = fma(wgt, vy, D.pi);
+    D.ir = fma(qb, vx, D.ir);
+    D.ii = fma(qb, vy, D.ii);
+    if (a == 0 && col == 0) {
+      D.g0r = vx;
+      D.g0i = vy;
+    }
+  }
+}
+
+template <int N, int S, int NT, int PAIRS, int NTHR>
+struct FftDifDigest {
+  __device__ __forceinline__ static void run(double2* T, const double2* rou_s, int tid, int bar,
+                                             int C, int ncol, int ncomp, const double* betaw_s,
+                                             int a0, DigestAcc& D) {
+    constexpr int R = smallest_prime_factor(S);
+    if constexpr (R == S) {
+      fft_last_digest<N, R, NT, PAIRS>(T, tid, C, ncol, ncomp, betaw_s, a0, D);
+      stage_sync(bar, NTHR);
+    } else {
+      fft_stage_ct<N, R, S, NT, PAIRS, NTHR>(T, rou_s, tid);
+      stage_sync(bar, NTHR);
+      FftDifDigest<N, S / R, NT, PAIRS, NTHR>::run(T, rou_s, tid, bar, C, ncol, ncomp, betaw_s, a0,
+                                                     D);
+    }
+  }
+};
+
+template <int N>
+__global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const LnParams LP) {
+  using Cfg = LnCfg<N>;
   constexpr int L = Cfg::L, MT = Cfg::MT, NT = Cfg::NT, NC = Cfg::NC, NPQ = Cfg::NPQ;
+  constexpr int NCW = Cfg::NCW, R1 = Cfg::R1, MP = Cfg::MP;
   const CoupleParams& P = LP.c;
   extern __shared__ __align__(128) unsigned char smem[];
   double2* Us = reinterpret_cast<double2*>(smem);
@@ -68,252 +199,282 @@ __global__ void __launch_bounds__(LnCfg<N, NWARP>::NTHREADS, 1) k_couple_lines(c
   double2* Tb = reinterpret_cast<double2*>(smem + Cfg::OFF_T);
   double2* rou_s = reinterpret_cast<double2*>(smem + Cfg::OFF_TAB);
   double* betaw_s = reinterpret_cast<double*>(rou_s + N);
-  int* perm_s = reinterpret_cast<int*>(betaw_s + (L + 1));
-  int* qoff_s = perm_s + N;
-  int* urb_s = qoff_s + (N + 1) + 1;
+  int* qoff_s = reinterpret_cast<int*>(betaw_s + (L + 1));
+  int* urb_s = qoff_s + (N + 2);
   CompRec* rec_s = reinterpret_cast<CompRec*>(
       (reinterpret_cast<uintptr_t>(urb_s + N) + 15) & ~static_cast<uintptr_t>(15));
+  double* dpart = reinterpret_cast<double*>(rec_s + MT);  // [NPART][MT][8] digest partials
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* ufull = bars + 0;
   uint64_t* uempty = bars + 1;
-  uint64_t* wfull = bars + 2;   // [2]
+  uint64_t* wfull = bars + 2;   // [2] W tile slots
   uint64_t* wempty = bars + 4;  // [2]
+  uint64_t* tready = bars + 6;  // [2] per tile parity: FFT of the tile done
+  uint64_t* tfree = bars + 8;   // [2] per tile parity: stores of the tile done
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nct = P.n_col_tiles;
+  constexpr size_t TE = Cfg::T_BYTES / 16;  // complex per T buffer
+  constexpr size_t WE = Cfg::WS_BYTES / 16;
 
   for (int i = tid; i < N; i += Cfg::NTHREADS) {
     rou_s[i] = P.rou[i];
-    perm_s[i] = P.perm[i];
     urb_s[i] = LP.urb[i];
   }
   for (int i = tid; i <= N; i += Cfg::NTHREADS) qoff_s[i] = P.qoff[i];
   for (int i = tid; i <= L; i += Cfg::NTHREADS) betaw_s[i] = P.betaw[i];
-  {
-    // W rows past NPQ are read (times a zero U pad) by partial k-steps: keep them finite
-    double4* w4 = reinterpret_cast<double4*>(smem + Cfg::OFF_W);
-    for (size_t i = tid; i < 2 * Cfg::W_BYTES / 32; i += Cfg::NTHREADS)
-      w4[i] = make_double4(0.0, 0.0, 0.0, 0.0);
-  }
+  // W rows past NPQ are read (times a zero U pad) by partial k-steps: keep them finite
+  for (int i = tid; i < 2 * 4 * NT; i += Cfg::NTHREADS)
+    Wsb[(i / (4 * NT)) * WE + (size_t)NPQ * NT + i % (4 * NT)] = make_double2(0.0, 0.0);
   if (tid == 0) {
     mbar_init(ufull, 1);
-    mbar_init(uempty, NWARP);
+    mbar_init(uempty, NCW);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&wfull[b], 1);
-      mbar_init(&wempty[b], NWARP);
+      mbar_init(&wempty[b], NCW);
+      mbar_init(&tready[b], NCW);
+      mbar_init(&tfree[b], Cfg::NSW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == NWARP) {
+  if (warp == 0) {
     // ------------------------------------------------------------------ producer
     if (lane == 0) {
       uint32_t uphase = 0;
-      int wslot = 0;
-      uint32_t wphase = 0;
+      long long t = 0;
       for (int g = blockIdx.x; g < LP.n_groups; g += gridDim.x) {
         mbar_wait(uempty, uphase ^ 1);
         const uint32_t ub = (uint32_t)(LP.group_elems * 16);
         mbar_arrive_expect_tx(ufull, ub);
         bulk_g2s(Us, P.U + (size_t)g * LP.group_elems, ub, ufull);
         uphase ^= 1;
-        for (int ct = 0; ct < nct; ++ct) {
-          mbar_wait(&wempty[wslot], wphase ^ 1);
-          const uint32_t wb = (uint32_t)(NPQ * NT * 16);
-          mbar_arrive_expect_tx(&wfull[wslot], wb);
-          bulk_g2s(Wsb + (size_t)wslot * (Cfg::W_BYTES / 16), P.W + (size_t)ct * NPQ * NT, wb,
-                   &wfull[wslot]);
-          if (++wslot == 2) {
-            wslot = 0;
-            wphase ^= 1;
-          }
+        for (int ct = 0; ct < nct; ++ct, ++t) {
+          const int sl = (int)(t & 1);
+          mbar_wait(&wempty[sl], (uint32_t)(((t >> 1) & 1) ^ 1));
+          constexpr uint32_t wb = (uint32_t)(NPQ * NT * 16);
+          mbar_arrive_expect_tx(&wfull[sl], wb);
+          bulk_g2s(Wsb + sl * WE, P.W + (size_t)ct * NPQ * NT, wb, &wfull[sl]);
         }
       }
     }
     return;
   }
 
-  // ------------------------------------------------------------------ consumers
-  const int kl = lane & 3;
-  uint32_t uphase = 0;
-  int wslot = 0;
-  uint32_t wphase = 0;
-  const long long vol = P.vol;
-  const int ncol = P.ncol;
-  for (int g = blockIdx.x; g < LP.n_groups; g += gridDim.x) {
-    const int comp0 = g * MT;
-    const int ncomp = min(MT, P.count - comp0);
-    if (tid < MT) rec_s[tid] = (tid < ncomp) ? P.comps[comp0 + tid] : CompRec{0, 0, -1, -1};
-    mbar_wait(ufull, uphase);
-    uphase ^= 1;
-    // digest accumulators: warp c < MT owns component c for the whole group
-    double s2 = 0.0, pr = 0.0, pi = 0.0, ir = 0.0, ii = 0.0, g0r = 0.0, g0i = 0.0;
-    long long mx2 = 0;
-    named_sync(1, NC);  // rec_s visible
-    for (int ct = 0; ct < nct; ++ct) {
-      const int C = ct * NT;
-      const int tb = ct == 0 ? 2 : (ct & 1);
-      const int tprev = ct == 1 ? 2 : ((ct - 1) & 1);
-      double2* T = Tb + (size_t)tb * (Cfg::T_BYTES / 16);
+  if (warp <= NCW) {
+    // ------------------------------------------------------------------ compute warps
+    const int cw = warp - 1;  // row group: T rows cw + k MP, k < R1 (one first-stage butterfly)
+    const int c_tid = tid - 32;
+    const int kl = lane & 3, ar = lane >> 2;
+    // per row of the group: its q row, k-steps, U and W offsets
+    int nks[R1], gr[R1], uo[R1];
+#pragma unroll
+    for (int k = 0; k < R1; ++k) {
+      const int x = cw + k * MP;                   // T row = q mod n
+      const int jq = x <= L ? x + L : x - L - 1;  // q + L
+      nks[k] = (L + 1 - abs(jq - L) + 3) >> 2;
+      gr[k] = qoff_s[jq];
+      uo[k] = ar * Cfg::UPAD + urb_s[jq] + kl;
+    }
+    const int a0 = dif_last_freq0<N, Cfg::RLAST>(c_tid / (MT * NT));
+    uint32_t uphase = 0;
+    long long t = 0;  // global tile counter of this CTA
+    for (int g = blockIdx.x; g < LP.n_groups; g += gridDim.x) {
+      const int ncomp = min(MT, P.count - g * MT);
+      DigestAcc D{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0};
+      mbar_wait(ufull, uphase);
+      uphase ^= 1;
+      for (int ct = 0; ct < nct; ++ct, ++t) {
+        double2* T = Tb + (size_t)(t % 3) * TE;
 #ifdef SLSHT_WS_TRACE
-      const bool tr = LP.trace && blockIdx.x == 0 && tid == 0 && g == 0 && ct < 64;
-      if (tr) LP.trace[ct * 6 + 0] = clock64();
+        const bool tr = LP.trace && blockIdx.x == 0 && c_tid == 0 && t < 128;
+        if (tr) LP.trace[t * 8 + 0] = clock64();
 #endif
-      // ---------------- MMA: one item per q row, NWARP warps
-      mbar_wait(&wfull[wslot], wphase);
+        // buffer t % 3 was last read by the stores of tile t-2 (as their previous tile)
+        if (t >= 2) mbar_wait(&tfree[t & 1], (uint32_t)(((t - 2) >> 1) & 1));
 #ifdef SLSHT_WS_TRACE
-      if (tr) LP.trace[ct * 6 + 1] = clock64();
+        if (tr) LP.trace[t * 8 + 1] = clock64();
 #endif
-      const double2* Ws = Wsb + (size_t)wslot * (Cfg::W_BYTES / 16);
-      for (int jq = warp; jq < N; jq += NWARP) {
-        const int np = L + 1 - abs(jq - L);
-        const int nks = (np + 3) >> 2;
-        const int wrb = qoff_s[jq];
-        const int ar = lane >> 2;
-        const int blo = lane >> 2;
-        const double2* ap = Us + ar * Cfg::UPAD + urb_s[jq] + kl;
-        const double2* bp = Ws + (wrb + kl) * NT + (blo ^ ((2 * (wrb + kl)) & 7));
-        double c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0}, c3[2] = {0.0, 0.0};
-        double2 a = ap[0], b = bp[0];
-        for (int ks = 0; ks < nks; ++ks) {
-          const int kn = min(ks + 1, nks - 1);
-          const double2 na = ap[4 * kn], nb = bp[4 * kn * NT];
-          dmma(c1[0], c1[1], a.x + a.y, b.x);
-          dmma(c2[0], c2[1], a.x, b.y - b.x);
-          dmma(c3[0], c3[1], a.y, b.x + b.y);
-          a = na;
-          b = nb;
+        const int sl = (int)(t & 1);
+        mbar_wait(&wfull[sl], (uint32_t)((t >> 1) & 1));
+#ifdef SLSHT_WS_TRACE
+        if (tr) LP.trace[t * 8 + 2] = clock64();
+#endif
+        const double2* Ws = Wsb + sl * WE;
+        // R1 independent DMMA chains (Gauss 3-product complex MMA), fully unrolled over k-steps
+        double c1[R1][2], c2[R1][2], c3[R1][2];
+#pragma unroll
+        for (int k = 0; k < R1; ++k) c1[k][0] = c1[k][1] = c2[k][0] = c2[k][1] = c3[k][0] = c3[k][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < Cfg::KSMAX; ++ks)
+#pragma unroll
+          for (int k = 0; k < R1; ++k)
+            if (ks < nks[k]) {
+              const int wr = gr[k] + 4 * ks + kl;
+              const double2 a = Us[uo[k] + 4 * ks];
+              const double2 b = Ws[wr * NT + (ar ^ ((2 * wr) & 7))];
+              dmma(c1[k][0], c1[k][1], a.x + a.y, b.x);
+              dmma(c2[k][0], c2[k][1], a.x, b.y - b.x);
+              dmma(c3[k][0], c3[k][1], a.y, b.x + b.y);
+            }
+#ifdef SLSHT_WS_TRACE
+        if (tr) LP.trace[t * 8 + 3] = clock64();
+#endif
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&wempty[sl]);
+        if (ct == nct - 1 && lane == 0) mbar_arrive(uempty);
+        // first DIF stage (radix R1, span N) on the accumulators: rows cw + k MP, twiddle
+        // rou^(cw k)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double xr[R1], xi[R1];
+#pragma unroll
+          for (int k = 0; k < R1; ++k) {
+            xr[k] = c1[k][e] - c3[k][e];
+            xi[k] = c1[k][e] + c2[k][e];
+          }
+          Radix<R1>::dft(xr, xi);
+          double2* dst = T + (size_t)(ar * N + cw) * NT + 2 * kl + e;
+          dst[0] = make_double2(xr[0], xi[0]);
+#pragma unroll
+          for (int k = 1; k < R1; ++k) {
+            const double2 w = rou_s[cw * k];
+            dst[(size_t)k * MP * NT] =
+                make_double2(xr[k] * w.x - xi[k] * w.y, xr[k] * w.y + xi[k] * w.x);
+          }
         }
-        const int row = jq >= L ? jq - L : jq + L + 1;  // q mod n
-        double2* dst = T + (size_t)(ar * N + row) * NT + 2 * kl;
-        dst[0] = make_double2(c1[0] - c3[0], c1[0] + c2[0]);
-        dst[1] = make_double2(c1[1] - c3[1], c1[1] + c2[1]);
-      }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&wempty[wslot]);
-        if (ct == nct - 1) mbar_arrive(uempty);
-      }
-      if (++wslot == 2) {
-        wslot = 0;
-        wphase ^= 1;
-      }
-      named_sync(1, NC);
 #ifdef SLSHT_WS_TRACE
-      if (tr) LP.trace[ct * 6 + 2] = clock64();
+        if (tr) LP.trace[t * 8 + 4] = clock64();
 #endif
-      // ---------------- alpha FFT of the tile, in place
-      FftDif<N, N, NT, MT * NT, NC>::run(T, rou_s, tid, 1);
+        named_sync(1, NC);
 #ifdef SLSHT_WS_TRACE
-      if (tr) LP.trace[ct * 6 + 3] = clock64();
+        if (tr) LP.trace[t * 8 + 5] = clock64();
 #endif
-      // ---------------- digest of the tile's own samples (warp c: component c)
-      if (warp < ncomp) {
-        const int c = warp;
-        const double2* Tc = T + (size_t)c * N * NT;
-        for (int v = lane; v < N * NT; v += 32) {
-          const int a = v / NT, j = v % NT, col = C + j;
-          if (col >= ncol) continue;
-          const double2 x = Tc[perm_s[a] * NT + j];
-          const double a2 = fma(x.x, x.x, x.y * x.y);
-          s2 += a2;
-          mx2 = max(mx2, __double_as_longlong(a2));
-          const uint32_t hsh = (uint32_t)((size_t)a * ncol + col) * 0x9E3779B1u;
-          const double wgt = digest_weight(hsh);
-          pr = fma(wgt, x.x, pr);
-          pi = fma(wgt, x.y, pi);
-          const double qb = betaw_s[col / N];
-          ir = fma(qb, x.x, ir);
-          ii = fma(qb, x.y, ii);
-          if (a == 0 && col == 0) {
-            g0r = x.x;
-            g0i = x.y;
+        FftDifDigest<N, MP, NT, MT * NT, NC>::run(T, rou_s, c_tid, 1, ct * NT, P.ncol, ncomp,
+                                                  betaw_s, a0, D);  // ends with a sync
+#ifdef SLSHT_WS_TRACE
+        if (tr) LP.trace[t * 8 + 6] = clock64();
+#endif
+        if (lane == 0) mbar_arrive(&tready[t & 1]);
+      }
+      // ---------------- digest rows of the group: 8-lane shuffle tree, then NPART partials
+      {
+        constexpr int LI = Cfg::LAST_ITEMS;  // thread c_tid < LI holds pair c_tid % 64
+        const unsigned m8 = 0xffu << (lane & ~7);
+        double v[8] = {D.s2, __longlong_as_double(D.mx2), D.pr, D.pi, D.g0r, D.g0i, D.ir, D.ii};
+        if (c_tid >= LI) {
+#pragma unroll
+          for (int f = 0; f < 8; ++f) v[f] = 0.0;
+        }
+#pragma unroll
+        for (int off = 4; off > 0; off >>= 1)
+#pragma unroll
+          for (int f = 0; f < 8; ++f) {
+            const double o = __shfl_down_sync(m8, v[f], off, 8);
+            v[f] = (f == 1) ? fmax(v[f], o) : v[f] + o;
+          }
+        if ((lane & 7) == 0 && c_tid < LI) {
+          const int c = (c_tid % (MT * NT)) / NT, ip = c_tid / (MT * NT);
+#pragma unroll
+          for (int f = 0; f < 8; ++f) dpart[(ip * MT + c) * 8 + f] = v[f];
+        }
+        named_sync(1, NC);
+        if (c_tid < ncomp * 8) {
+          const int c = c_tid >> 3, f = c_tid & 7;
+          double s = 0.0;
+#pragma unroll
+          for (int ip = 0; ip < Cfg::NPART; ++ip) {
+            const double x = dpart[(ip * MT + c) * 8 + f];
+            s = (f == 1) ? fmax(s, x) : s + x;
+          }
+          const CompRec rec = P.comps[g * MT + c];
+          if (f == 1) s = sqrt(s);
+          if (f >= 6) s *= 1.0 / ((double)N * N * N);
+          LP.digest[(size_t)(rec.l * rec.l + rec.l + rec.m) * 8 + f] = s;
+          if (P.mirror && rec.m > 0) {
+            const double sg = (rec.m & 1) ? -1.0 : 1.0;
+            const double sm = f < 2 ? s : ((f & 1) ? -(sg * s) : sg * s);  // (-1)^m conj
+            LP.digest[(size_t)(rec.l * rec.l + rec.l - rec.m) * 8 + f] = sm;
+          }
+        }
+        named_sync(1, NC);  // dpart reused by the next group
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ store warps
+  // line group g8 = (component c, volume w): for every row a of tile ct the aligned 128-B line
+  // that starts in (p0 - 8, p0], p0 = the row's first element in the tile. Row a starts at
+  // base + a ncol, ncol == 1 (mod 8), so the line phase of row a is (base + a) & 7.
+  constexpr DifPerm<N> kPerm{};
+  const int st = tid - 32 - NC;  // 0 .. NSW*32-1
+  const int j = st & 7;          // element of the line
+  const int g8 = st >> 3;
+  const int c = g8 & 7, w = g8 >> 3;
+  const int ncol = P.ncol;
+  const long long sbit = (long long)0x8000000000000000ULL;
+  long long t = 0;
+  for (int g = blockIdx.x; g < LP.n_groups; g += gridDim.x) {
+    const int ncomp = min(MT, P.count - g * MT);
+    bool act = c < ncomp;
+    long long base = 0;
+    long long fr = 0, fi = 0;
+    if (act) {
+      const CompRec rec = P.comps[g * MT + c];
+      act = (w == 0) || (P.mirror && rec.m > 0);
+      base = (w ? rec.mslot : rec.slot) * P.vol;
+      if (w) {  // (-1)^m conj
+        fr = (rec.m & 1) ? sbit : 0;
+        fi = (rec.m & 1) ? 0 : sbit;
+      }
+    }
+    const int ksh0 = (int)(base & 7);
+    double2* outp = P.out + base;
+    for (int ct = 0; ct < nct; ++ct, ++t) {
+      const int C = ct * NT;
+      mbar_wait(&tready[t & 1], (uint32_t)((t >> 1) & 1));
+#ifdef SLSHT_WS_TRACE
+      const bool tr = LP.trace && blockIdx.x == 0 && st == 0 && t < 128;
+#endif
+#ifndef LN_NO_STORE
+      if (act) {
+        const double2* Tc = Tb + (size_t)(t % 3) * TE + (size_t)c * N * NT;
+        const double2* Tp = Tb + (size_t)((t + 2) % 3) * TE + (size_t)c * N * NT + 8;
+        double2* orow = outp + C;  // row a: orow + a ncol
+        if (ct > 0 && ct < nct - 1) {
+          // interior tile: every element of every line exists
+#pragma unroll
+          for (int a = 0; a < N; ++a) {
+            const int d = j - ((ksh0 + a) & 7);  // column offset from C (< 0: previous tile)
+            const double2* src = (d < 0 ? Tp : Tc) + kPerm.v[a] * NT + d;
+            double2 v = *src;
+            v = make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ fr),
+                             __longlong_as_double(__double_as_longlong(v.y) ^ fi));
+            orow[a * ncol + d] = v;
+          }
+        } else {
+          const int cmax = ncol - C;  // columns of this tile in the row
+#pragma unroll
+          for (int a = 0; a < N; ++a) {
+            const int d = j - ((ksh0 + a) & 7);
+            if (d >= 0 ? d < cmax : ct > 0) {
+              const double2* src = (d < 0 ? Tp : Tc) + kPerm.v[a] * NT + d;
+              double2 v = *src;
+              v = make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ fr),
+                               __longlong_as_double(__double_as_longlong(v.y) ^ fi));
+              orow[a * ncol + d] = v;
+            }
           }
         }
       }
-#ifdef SLSHT_WS_TRACE
-      if (tr) LP.trace[ct * 6 + 4] = clock64();
 #endif
-      // ---------------- aligned line stores: job = (component, row, volume) -> one 128-B line
-      const double2* Tcur = T;
-      const double2* Tprv = Tb + (size_t)tprev * (Cfg::T_BYTES / 16);
-      const double2* T0 = Tb + (size_t)2 * (Cfg::T_BYTES / 16);
-      const bool last = ct == nct - 1;
-      const int n_jobs = MT * N * (P.mirror ? 2 : 1);
-      for (int job = (tid >> 3); job < n_jobs; job += NC / 8) {
-        const int j = tid & 7;
-        const int which = job / (MT * N);  // 0: the component, 1: its conjugate mirror
-        const int r = job % (MT * N);
-        const int c = r / N, a = r % N;
-        if (c >= ncomp) continue;
-        const CompRec rec = rec_s[c];
-        if (which == 1 && !(rec.m > 0)) continue;
-        const long long base = (which ? rec.mslot : rec.slot) * vol;  // volume start
-        const long long rowp = base + (long long)a * ncol;            // row start
-        const long long p0 = rowp + C;
-        const long long e = p0 + ((7 - (p0 & 7)) & 7);  // the line's last element
-        const long long s = e - 7;
-        if (ct == 0 && s < rowp && a > 0) continue;  // written with row a-1's last tile
-        const long long x = s + j;                    // this lane's element
-        if (x < base || x >= base + vol) continue;    // partial line at a volume end
-        const int d = (int)(x - rowp);                // column within row a (may run past it)
-        double2 v;
-        if (d >= ncol) {
-          v = T0[(size_t)(c * N + perm_s[a + 1]) * NT + (d - ncol)];  // next row's head (tile 0)
-        } else if (d >= C) {
-          v = Tcur[(size_t)(c * N + perm_s[a]) * NT + (d - C)];
-        } else {
-          v = Tprv[(size_t)(c * N + perm_s[a]) * NT + (d - (C - NT))];
-        }
-        if (which) {
-          const long long sbit = (long long)0x8000000000000000ULL;
-          const long long fr = (rec.m & 1) ? sbit : 0, fi = (rec.m & 1) ? 0 : sbit;
-          v = make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ fr),
-                           __longlong_as_double(__double_as_longlong(v.y) ^ fi));
-        }
-        P.out[x] = v;
-        (void)last;
-      }
-      named_sync(1, NC);  // T buffers reused by the next tiles
 #ifdef SLSHT_WS_TRACE
-      if (tr) LP.trace[ct * 6 + 5] = clock64();
+      if (tr) LP.trace[t * 8 + 7] = clock64();
 #endif
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tfree[t & 1]);
     }
-    // ---------------- digest rows of the group
-    if (warp < ncomp) {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        s2 += __shfl_down_sync(0xffffffffu, s2, off);
-        mx2 = max(mx2, (long long)__shfl_down_sync(0xffffffffu, (unsigned long long)mx2, off));
-        pr += __shfl_down_sync(0xffffffffu, pr, off);
-        pi += __shfl_down_sync(0xffffffffu, pi, off);
-        ir += __shfl_down_sync(0xffffffffu, ir, off);
-        ii += __shfl_down_sync(0xffffffffu, ii, off);
-        g0r += __shfl_down_sync(0xffffffffu, g0r, off);
-        g0i += __shfl_down_sync(0xffffffffu, g0i, off);
-      }
-      if (lane == 0) {
-        const CompRec rec = rec_s[warp];
-        const double inv = 1.0 / ((double)N * N * N);
-        double d[8] = {s2, sqrt(__longlong_as_double(mx2)), pr, pi, g0r, g0i, ir * inv, ii * inv};
-        double* dst = LP.digest + (size_t)(rec.l * rec.l + rec.l + rec.m) * 8;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) dst[k] = d[k];
-        if (P.mirror && rec.m > 0) {
-          const double sg = (rec.m & 1) ? -1.0 : 1.0;
-          double* dm = LP.digest + (size_t)(rec.l * rec.l + rec.l - rec.m) * 8;
-          dm[0] = d[0];
-          dm[1] = d[1];
-          dm[2] = sg * d[2];
-          dm[3] = -(sg * d[3]);
-          dm[4] = sg * d[4];
-          dm[5] = -(sg * d[5]);
-          dm[6] = sg * d[6];
-          dm[7] = -(sg * d[7]);
-        }
-      }
-    }
-    named_sync(1, NC);  // rec_s reused by the next group
   }
 }
 

@@ -292,23 +292,49 @@ void build_plan(slsht_cuda_plan* p) {
   p->n_nodes = p->N + 1;
   p->ldA = (p->n_nodes + MG_K - 1) / MG_K * MG_K;
   p->vol = (long long)p->n * p->n * p->nb;
+  // ---- component list: orders m (all or m >= 0 in real mode), degrees in the shard
+  for (int m = p->real_mode ? 0 : -p->lmax; m <= p->lmax; ++m) {
+    const int lo = std::max(std::abs(m), p->l_begin), hi = std::min(p->lmax, p->l_end - 1);
+    for (int l = lo; l <= hi; ++l) p->comps.push_back(CompRec{l, m, 0, -1});
+  }
+  const long long total = (long long)p->comps.size();
+  p->emitted = 0;
+  for (const auto& c : p->comps) p->emitted += (p->mirror && c.m > 0) ? 2 : 1;
+
+  // ---- chunking and output slots
+  const size_t vol_bytes = (size_t)p->vol * 16;
+  if (p->materialize) {
+    p->slot_base = (long long)p->l_begin * p->l_begin;
+    p->n_slots = (long long)p->l_end * p->l_end - p->slot_base;
+    p->max_chunk = (int)std::min<long long>(std::max<long long>(total, 1), 16384);
+  } else {
+    long long ring = d.ring_bytes > 0 ? d.ring_bytes : (1LL << 31);
+    const int per = p->mirror ? 2 : 1;
+    long long ch = ring / (2LL * per * (long long)vol_bytes);
+    ch = std::max<long long>(8, ch / 8 * 8);
+    ch = std::min<long long>(ch, 16384);
+    ch = std::min<long long>(ch, std::max<long long>(8, (total + 7) / 8 * 8));
+    p->max_chunk = (int)ch;
+    p->n_slots = 2LL * per * ch;
+  }
   couple_tile(p->n, p->MG, p->NG);
-  if (std::getenv("SLSHT_CUDA_LINES") != nullptr && (p->ncol % 8) == 1 &&
-      (p->n == 17 || p->n == 33)) {
+  // line-aligned kernel: whole component groups per CTA, so it needs enough groups per chunk
+  // to balance over the SMs (B200: 148); SLSHT_CUDA_LINES=0/1 forces it off/on
+  bool lines = false;
+  if ((p->ncol % 8) == 1 && p->n == 33) {
+    const long long groups = (p->max_chunk + 7) / 8, sms = 148;
+    const double eff = (double)groups / (double)(((groups + sms - 1) / sms) * sms);
+    lines = eff >= 0.85;
+    if (const char* e = std::getenv("SLSHT_CUDA_LINES")) lines = e[0] == '1';
+  }
+  if (lines) {
     p->use_lines = true;
     p->MG = 1;
     p->NG = 1;
-    if (p->n == 17) {
-      p->lines_fn = k_couple_lines<17, 16>;
-      p->lines_threads = LnCfg<17, 16>::NTHREADS;
-      p->couple_smem = LnCfg<17, 16>::SMEM;
-      p->lines_upad = LnCfg<17, 16>::UPAD;
-    } else {
-      p->lines_fn = k_couple_lines<33, 16>;
-      p->lines_threads = LnCfg<33, 16>::NTHREADS;
-      p->couple_smem = LnCfg<33, 16>::SMEM;
-      p->lines_upad = LnCfg<33, 16>::UPAD;
-    }
+    p->lines_fn = k_couple_lines<33>;
+    p->lines_threads = LnCfg<33>::NTHREADS;
+    p->couple_smem = LnCfg<33>::SMEM;
+    p->lines_upad = LnCfg<33>::UPAD;
   } else if (std::getenv("SLSHT_CUDA_NO_WS") == nullptr && ws_kernel(p->n, p->ws)) {
     p->use_ws = true;
     p->MG = p->ws.MT / 8;
@@ -444,31 +470,6 @@ void build_plan(slsht_cuda_plan* p) {
     for (int a = 0; a < n; ++a) perm[a] = a;
   }
 
-  // ---- component list: orders m (all or m >= 0 in real mode), degrees in the shard
-  for (int m = p->real_mode ? 0 : -p->lmax; m <= p->lmax; ++m) {
-    const int lo = std::max(std::abs(m), p->l_begin), hi = std::min(p->lmax, p->l_end - 1);
-    for (int l = lo; l <= hi; ++l) p->comps.push_back(CompRec{l, m, 0, -1});
-  }
-  const long long total = (long long)p->comps.size();
-  p->emitted = 0;
-  for (const auto& c : p->comps) p->emitted += (p->mirror && c.m > 0) ? 2 : 1;
-
-  // ---- chunking and output slots
-  const size_t vol_bytes = (size_t)p->vol * 16;
-  if (p->materialize) {
-    p->slot_base = (long long)p->l_begin * p->l_begin;
-    p->n_slots = (long long)p->l_end * p->l_end - p->slot_base;
-    p->max_chunk = (int)std::min<long long>(std::max<long long>(total, 1), 16384);
-  } else {
-    long long ring = d.ring_bytes > 0 ? d.ring_bytes : (1LL << 31);
-    const int per = p->mirror ? 2 : 1;
-    long long ch = ring / (2LL * per * (long long)vol_bytes);
-    ch = std::max<long long>(8, ch / 8 * 8);
-    ch = std::min<long long>(ch, 16384);
-    ch = std::min<long long>(ch, std::max<long long>(8, (total + 7) / 8 * 8));
-    p->max_chunk = (int)ch;
-    p->n_slots = 2LL * per * ch;
-  }
   for (long long c0 = 0, ci = 0; c0 < total; c0 += p->max_chunk, ++ci) {
     Chunk ch{};
     ch.comp0 = c0;
@@ -669,20 +670,22 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     const int grid = std::min(lp.n_groups, p->num_sms);
 #ifdef SLSHT_WS_TRACE
     static long long* d_ltrace = nullptr;
-    if (!d_ltrace) CK(cudaMalloc(&d_ltrace, 2048 * sizeof(long long)));
-    CK(cudaMemsetAsync(d_ltrace, 0, 2048 * sizeof(long long), s));
+    if (!d_ltrace) CK(cudaMalloc(&d_ltrace, 1024 * sizeof(long long)));
+    CK(cudaMemsetAsync(d_ltrace, 0, 1024 * sizeof(long long), s));
     lp.trace = d_ltrace;
 #endif
     p->lines_fn<<<grid, p->lines_threads, p->couple_smem, s>>>(lp);
 #ifdef SLSHT_WS_TRACE
     {
-      long long h[64 * 6];
+      long long h[1024];
       CK(cudaMemcpyAsync(h, d_ltrace, sizeof(h), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      for (int k = 0; k < 8; ++k)
-        fprintf(stderr, "lines tile %2d: start %8lld wwait %6lld mma %6lld fft %6lld digest %6lld lines %6lld\n",
-                k, h[6 * k] - h[0], h[6 * k + 1] - h[6 * k], h[6 * k + 2] - h[6 * k + 1],
-                h[6 * k + 3] - h[6 * k + 2], h[6 * k + 4] - h[6 * k + 3], h[6 * k + 5] - h[6 * k + 4]);
+      fprintf(stderr, "lines grid %d groups %d\n", grid, lp.n_groups);
+      for (int k = 0; k < 80; ++k) {
+        const long long* r = h + 8 * k;
+        fprintf(stderr, "tile %3d: start %8lld tfree %5lld wfull %5lld mma %5lld radix %5lld sync %5lld last %5lld | stores_done %8lld\n",
+                k, r[0] - h[0], r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4], r[6] - r[5], r[7] - h[0]);
+      }
     }
 #endif
   } else if (p->use_ws) {
