@@ -8,55 +8,61 @@ namespace slsht_cuda {
 
 // ---------------------------------------------------------------------------------------------
 // Setup: theta nodes of S_{2L_g}, theta_weights(2L_g) (grids.cpp:76-92), beta_weights(L_h)
-// (grids.cpp:54-74). One thread per node; the k-sums run in the reference's order.
+// (grids.cpp:54-74). One warp per weight: lanes take the k terms of the quadrature sum
+// (only w(0), w(+-1) and even k are nonzero) and a fixed shuffle tree adds them, so the result
+// is deterministic (it differs from the reference's serial k order by roundoff only).
+__device__ __forceinline__ void quad_weight_sum(int K, double angle, int lane, double& sr,
+                                                double& si) {
+  sr = 0.0;
+  si = 0.0;
+  for (int k = -K + lane; k <= K; k += 32) {
+    const int mk = -k;
+    double wr = 0.0, wi = 0.0;
+    if (mk == 0) wr = 2.0;
+    else if (mk == 1) wi = kPi / 2.0;
+    else if (mk == -1) wi = -kPi / 2.0;
+    else if ((mk & 1) == 0) wr = 2.0 / (1.0 - (double)mk * mk);
+    if (wr == 0.0 && wi == 0.0) continue;
+    const double ck = cos(k * angle);
+    sr += wr * ck;
+    si += wi * ck;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    sr += __shfl_xor_sync(0xffffffffu, sr, off);
+    si += __shfl_xor_sync(0xffffffffu, si, off);
+  }
+}
+
 __global__ void k_nodes(int N, double* __restrict__ ncos, double* __restrict__ nsin,
                         double* __restrict__ weights, int L_h, double* __restrict__ betaw,
                         int* __restrict__ err_flag) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t <= N) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w <= N) {
+    const int t = w;
     const double theta = kPi * (2 * t + 1) / (2 * N + 1);
-    double s, c;
-    sincos(theta, &s, &c);
-    ncos[t] = c;
-    nsin[t] = s;
-    // sum_k w(-k) cos(k theta); only w(0) and even k have real parts, w(+-1) are imaginary
-    double sr = 0.0, si = 0.0;
-    for (int k = -N; k <= N; ++k) {
-      const int mk = -k;
-      double wr = 0.0, wi = 0.0;
-      if (mk == 0) wr = 2.0;
-      else if (mk == 1) wi = kPi / 2.0;
-      else if (mk == -1) wi = -kPi / 2.0;
-      else if ((mk & 1) == 0) wr = 2.0 / (1.0 - (double)mk * mk);
-      if (wr == 0.0 && wi == 0.0) continue;
-      const double ck = cos(k * theta);
-      sr += wr * ck;
-      si += wi * ck;
+    double sr, si;
+    quad_weight_sum(N, theta, lane, sr, si);
+    if (lane == 0) {
+      double s, c;
+      sincos(theta, &s, &c);
+      ncos[t] = c;
+      nsin[t] = s;
+      if (fabs(si) >= 1e-12) atomicExch(err_flag, 1);
+      weights[t] = (t < N) ? 2.0 * sr / (2 * N + 1) : sr / (2 * N + 1);
     }
-    if (fabs(si) >= 1e-12) atomicExch(err_flag, 1);
-    weights[t] = (t < N) ? 2.0 * sr / (2 * N + 1) : sr / (2 * N + 1);
-  }
-  if (t <= L_h) {
+  } else if (w - (N + 1) <= L_h) {
+    const int t = w - (N + 1);
     const int L = L_h, n = 2 * L + 1;
     if (t == 0) {
-      betaw[0] = 4.0 * kPi * kPi / (L / 2 + 0.5);
+      if (lane == 0) betaw[0] = 4.0 * kPi * kPi / (L / 2 + 0.5);
     } else {
-      const double beta = 2.0 * kPi * t / n;
-      double sr = 0.0, si = 0.0;
-      for (int m = -L; m <= L; ++m) {
-        const int mm = -m;
-        double wr = 0.0, wi = 0.0;
-        if (mm == 0) wr = 2.0;
-        else if (mm == 1) wi = kPi / 2.0;
-        else if (mm == -1) wi = -kPi / 2.0;
-        else if ((mm & 1) == 0) wr = 2.0 / (1.0 - (double)mm * mm);
-        if (wr == 0.0 && wi == 0.0) continue;
-        const double cm = cos(m * beta);
-        sr += wr * cm;
-        si += wi * cm;
+      double sr, si;
+      quad_weight_sum(L, 2.0 * kPi * t / n, lane, sr, si);
+      if (lane == 0) {
+        if (fabs(si) >= 1e-12) atomicExch(err_flag, 2);
+        betaw[t] = 8.0 * kPi * kPi * sr;
       }
-      if (fabs(si) >= 1e-12) atomicExch(err_flag, 2);
-      betaw[t] = 8.0 * kPi * kPi * sr;
     }
   }
 }
@@ -84,15 +90,18 @@ __global__ void k_legendre_window(int L_h, int n_nodes, const double* __restrict
 }
 
 // I(theta_j, mu) = 2 pi conj(sum_{l=|mu|}^{L_f} f_l^mu lambda_l^mu(theta_j)) (transform.cpp:158-173)
-// grid (node blocks, 2L_f+1 orders); dynamic smem 3 (L_f+1) doubles.
+// grid (node blocks, 2L_f+1 orders); dynamic smem 3 (L_f+1) doubles + (L_f+1) complex (f_l^mu).
 __global__ void k_itab(int L_f, int n_nodes, const double* __restrict__ ncos,
                        const double* __restrict__ nsin, const double* __restrict__ f,
                        double* __restrict__ itab) {
   extern __shared__ double coef[];
   double *sf = coef, *ca = coef + (L_f + 1), *cb = coef + 2 * (L_f + 1);
+  double2* fs = reinterpret_cast<double2*>(coef + 3 * (L_f + 1) + ((3 * (L_f + 1)) & 1));
   const int mu = (int)blockIdx.y - L_f;
   const int amu = mu < 0 ? -mu : mu;
   legendre_coeffs(amu, L_f, sf, ca, cb);
+  for (int l = amu + threadIdx.x; l <= L_f; l += blockDim.x)
+    fs[l] = *reinterpret_cast<const double2*>(f + 2 * (l * l + l + mu));
   __syncthreads();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n_nodes) return;
@@ -101,7 +110,7 @@ __global__ void k_itab(int L_f, int n_nodes, const double* __restrict__ ncos,
   double ar = 0.0, ai = 0.0;
   for (int l = amu; l <= L_f; ++l) {
     if (l > amu) r.next(ca, cb);
-    const double2 fv = *reinterpret_cast<const double2*>(f + 2 * (l * l + l + mu));
+    const double2 fv = fs[l];
     ar += fv.x * r.cur;
     ai += fv.y * r.cur;
   }
@@ -116,11 +125,18 @@ __global__ void k_itab(int L_f, int n_nodes, const double* __restrict__ ncos,
 // shared memory (downward three-term recursion per column, then transpose) and written to
 // global through the d-matrix symmetries. Explicit _rn intrinsics keep every operation
 // separately rounded (no FMA contraction), so the table is bit-identical to the reference.
+// PRE: the recursion coefficients of a level (a square root and a division per (m, m') --
+// the slow part) are computed by all threads before the recursion, so the serial chain of a
+// column is two multiplies and a subtraction per step. Shared memory: 2 S^2 + 2 S doubles
+// (PRE) or S^2 + S, S = L + 1.
+template <bool PRE>
 __global__ void k_delta(int L, double* __restrict__ delta) {
   extern __shared__ double sm[];
   const int S = L + 1;
   double* sec = sm;           // S x S sector [m][mp], m, mp >= 0
   double* top = sm + S * S;   // previous level's top row Delta^{l-1}_{l-1, mp}
+  double* ca = top + S;       // PRE: 2 mp / sqrt((l - m)(l + m + 1)) at [m][mp]
+  double* cc = ca + S * S;    // PRE: sqrt((l - m - 1)(l + m + 2)) / sqrt((l - m)(l + m + 1))
   const int tid = threadIdx.x;
   if (tid == 0) {
     delta[0] = 1.0;
@@ -142,15 +158,31 @@ __global__ void k_delta(int L, double* __restrict__ delta) {
       }
       sec[l * S + mp] = v;
     }
+    if constexpr (PRE) {
+      for (int idx = tid; idx < l * l; idx += blockDim.x) {
+        const int m = idx / l, mp = idx % l;
+        if (mp > m) continue;
+        const double denom = __dsqrt_rn(__dmul_rn((double)(l - m), l + m + 1.0));
+        ca[m * S + mp] = __ddiv_rn(2.0 * mp, denom);
+        if (mp == 0 && m + 2 <= l)
+          cc[m] = __ddiv_rn(__dsqrt_rn(__dmul_rn(l - m - 1.0, l + m + 2.0)), denom);
+      }
+    }
     __syncthreads();
     // downward recursion in m over the sector m >= mp >= 0, one column per thread
     for (int mp = tid; mp <= l - 1; mp += blockDim.x) {
       for (int m = l - 1; m >= mp; --m) {
-        const double denom = __dsqrt_rn(__dmul_rn((double)(l - m), l + m + 1.0));
-        double value = __dmul_rn(__ddiv_rn(2.0 * mp, denom), sec[(m + 1) * S + mp]);
-        if (m + 2 <= l) {
-          const double c2 = __ddiv_rn(__dsqrt_rn(__dmul_rn(l - m - 1.0, l + m + 2.0)), denom);
-          value = __dsub_rn(value, __dmul_rn(c2, sec[(m + 2) * S + mp]));
+        double value;
+        if constexpr (PRE) {
+          value = __dmul_rn(ca[m * S + mp], sec[(m + 1) * S + mp]);
+          if (m + 2 <= l) value = __dsub_rn(value, __dmul_rn(cc[m], sec[(m + 2) * S + mp]));
+        } else {
+          const double denom = __dsqrt_rn(__dmul_rn((double)(l - m), l + m + 1.0));
+          value = __dmul_rn(__ddiv_rn(2.0 * mp, denom), sec[(m + 1) * S + mp]);
+          if (m + 2 <= l) {
+            const double c2 = __ddiv_rn(__dsqrt_rn(__dmul_rn(l - m - 1.0, l + m + 2.0)), denom);
+            value = __dsub_rn(value, __dmul_rn(c2, sec[(m + 2) * S + mp]));
+          }
         }
         sec[m * S + mp] = value;
       }
@@ -178,6 +210,25 @@ __global__ void k_delta(int L, double* __restrict__ delta) {
     off += (size_t)w * w;
     __syncthreads();
   }
+}
+
+// Launch k_delta for band limit L on stream s (one CTA).
+inline cudaError_t launch_delta(int L, double* out, cudaStream_t s) {
+  const size_t S = (size_t)L + 1;
+  const size_t pre = sizeof(double) * (2 * S * S + 2 * S), plain = sizeof(double) * (S * S + S);
+  if (pre <= 227 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_delta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)pre);
+    if (e != cudaSuccess) return e;
+    k_delta<true><<<1, 256, pre, s>>>(L, out);
+  } else {
+    if (plain > 227 * 1024) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(k_delta<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plain);
+    if (e != cudaSuccess) return e;
+    k_delta<false><<<1, 256, plain, s>>>(L, out);
+  }
+  return cudaGetLastError();
 }
 
 __device__ __forceinline__ size_t delta_offset(int p) {

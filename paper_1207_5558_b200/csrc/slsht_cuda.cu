@@ -596,19 +596,17 @@ void run_setup(slsht_cuda_plan* p) {
   cudaStream_t s = p->stream;
   const int L = p->L_h;
   record(p, 0);
-  k_nodes<<<(p->n_nodes + 127) / 128, 128, 0, s>>>(p->N, p->d_ncos, p->d_nsin, p->d_weights, L,
-                                                   p->d_betaw, p->d_err);
+  k_nodes<<<(p->n_nodes + L + 1 + 3) / 4, 128, 0, s>>>(p->N, p->d_ncos, p->d_nsin, p->d_weights,
+                                                       L, p->d_betaw, p->d_err);  // warp per weight
   CKL();
   k_legendre_window<<<dim3((p->n_nodes + 127) / 128, p->n), 128, 3 * (L + 1) * sizeof(double), s>>>(
       L, p->n_nodes, p->d_ncos, p->d_nsin, p->d_qoff, p->d_lamh);
   CKL();
   k_itab<<<dim3((p->n_nodes + 127) / 128, 2 * p->L_f + 1), 128,
-           3 * (p->L_f + 1) * sizeof(double), s>>>(
+           (5 * (p->L_f + 1) + 1) * sizeof(double), s>>>(
       p->L_f, p->n_nodes, p->d_ncos, p->d_nsin, p->d_f, reinterpret_cast<double*>(p->d_itab));
   CKL();
-  const size_t dsm = sizeof(double) * ((size_t)(L + 1) * (L + 1) + (L + 1));
-  k_delta<<<1, 128, dsm, s>>>(L, p->d_delta);
-  CKL();
+  CK(launch_delta(L, p->d_delta, s));
   const int wmax = (2 * L + 1) * (2 * L + 1) * p->nb;
   k_dtab<<<dim3((wmax + 255) / 256, L + 1), 256, 0, s>>>(L, p->d_delta, p->d_rou, p->d_dtab);
   CKL();
@@ -990,9 +988,9 @@ int slsht_cuda_delta_tables(int device, int L, double* out) {
     size_t dsz = 0;
     for (int pp = 0; pp <= L; ++pp) dsz += (size_t)(2 * pp + 1) * (2 * pp + 1);
     double* d = dalloc<double>(dsz);
-    const size_t dsm = sizeof(double) * ((size_t)(L + 1) * (L + 1) + (L + 1));
-    k_delta<<<1, 128, dsm>>>(L, d);
-    CKL();
+    if ((size_t)(L + 1) * (L + 1) * 8 > 220 * 1024)
+      throw Status{SLSHT_ERR_VALIDATION, "band limit too large for the on-chip Delta recursion"};
+    CK(launch_delta(L, d, 0));
     CK(cudaMemcpy(out, d, dsz * sizeof(double), cudaMemcpyDeviceToHost));
     CK(cudaFree(d));
     return SLSHT_OK;
