@@ -110,6 +110,9 @@ struct slsht_cuda_plan {
   int* d_ustr = nullptr;   //   and row stride
   int ct_fast = 0;
   cudaStream_t stream = nullptr, copy_stream = nullptr;
+  cudaStream_t aux_stream = nullptr;  // window-table chain of the setup, overlapped
+  cudaEvent_t ev_fork = nullptr, ev_wtab = nullptr;
+  bool wtab_pending = false;
   bool own_stream = false;
   bool profile = false;
   std::string last_error;
@@ -190,6 +193,12 @@ void free_plan(slsht_cuda_plan* p) {
   for (auto& e : p->ev_stage)
     if (e) cudaEventDestroy(e);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->aux_stream) {
+    cudaStreamSynchronize(p->aux_stream);
+    cudaStreamDestroy(p->aux_stream);
+  }
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_wtab) cudaEventDestroy(p->ev_wtab);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -373,6 +382,9 @@ void build_plan(slsht_cuda_plan* p) {
     p->own_stream = true;
   }
   CK(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&p->aux_stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&p->ev_wtab, cudaEventDisableTiming));
   cudaStream_t s = p->stream;
 
   // ---- q-major (p, q) ordering of the window band: c = qoff[q+L] + p - |q|
@@ -591,11 +603,23 @@ void accumulate(slsht_cuda_plan* p, int st, int a, int b) {
   p->stage_ms[st] += ms;
 }
 
+// The main stream waits for the window-table chain (before the first coupling launch).
+void join_aux(slsht_cuda_plan* p) {
+  if (!p->wtab_pending) return;
+  CK(cudaStreamWaitEvent(p->stream, p->ev_wtab, 0));
+  p->wtab_pending = false;
+}
+
 // Setup stage: every table that depends on f, h or the band limits (recomputed per call).
+// Two independent chains: nodes -> Legendre window rows -> I table (needed by the modulated
+// SHT) on the main stream, and Delta -> d tables -> window table W (needed only by the
+// coupling) on the auxiliary stream, where it overlaps the node chain and the modulated SHT.
 void run_setup(slsht_cuda_plan* p) {
   cudaStream_t s = p->stream;
   const int L = p->L_h;
   record(p, 0);
+  CK(cudaEventRecord(p->ev_fork, s));  // after the inputs' upload on s
+  CK(cudaStreamWaitEvent(p->aux_stream, p->ev_fork, 0));
   k_nodes<<<(p->n_nodes + L + 1 + 3) / 4, 128, 0, s>>>(p->N, p->d_ncos, p->d_nsin, p->d_weights,
                                                        L, p->d_betaw, p->d_err);  // warp per weight
   CKL();
@@ -606,15 +630,18 @@ void run_setup(slsht_cuda_plan* p) {
            (5 * (p->L_f + 1) + 1) * sizeof(double), s>>>(
       p->L_f, p->n_nodes, p->d_ncos, p->d_nsin, p->d_f, reinterpret_cast<double*>(p->d_itab));
   CKL();
-  CK(launch_delta(L, p->d_delta, s));
+  cudaStream_t a = p->aux_stream;
+  CK(launch_delta(L, p->d_delta, a));
   const int wmax = (2 * L + 1) * (2 * L + 1) * p->nb;
-  k_dtab<<<dim3((wmax + 255) / 256, L + 1), 256, 0, s>>>(L, p->d_delta, p->d_rou, p->d_dtab);
+  k_dtab<<<dim3((wmax + 255) / 256, L + 1), 256, 0, a>>>(L, p->d_delta, p->d_rou, p->d_dtab);
   CKL();
   const int tile_nt = p->use_lines ? 8 : (p->use_ws ? p->ws.NT : 0);
   const int ncol_pad = tile_nt ? p->n_col_tiles * tile_nt : p->ncol;
-  k_wtab<<<dim3((ncol_pad + 127) / 128, p->NPQ), 128, 0, s>>>(L, p->d_h, p->d_dtab, p->d_rou,
+  k_wtab<<<dim3((ncol_pad + 127) / 128, p->NPQ), 128, 0, a>>>(L, p->d_h, p->d_dtab, p->d_rou,
                                                              p->d_pq, tile_nt, ncol_pad, p->d_W);
   CKL();
+  CK(cudaEventRecord(p->ev_wtab, a));
+  p->wtab_pending = true;
   p->launches += 6;
   record(p, 1);
   accumulate(p, ST_SETUP, 0, 1);
@@ -633,6 +660,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
       p->d_pq, p->use_lines ? 8 : (p->use_ws ? p->ws.MT : 0), p->ws_stages.group_elems,
       p->d_ubase, p->d_ustr, p->d_U);
   CKL();
+  join_aux(p);
   record(p, 2);
   CoupleParams prm{};
   prm.U = p->d_U;
@@ -840,6 +868,7 @@ int slsht_cuda_forward_device(slsht_cuda_plan* p, const double* f, const double*
     load_inputs(p, f, h, inputs_on_device != 0);
     run_setup(p);
     for (const Chunk& ch : p->chunks) run_chunk(p, ch);
+    join_aux(p);
     if (digests) copy_digests(p, digests, digests_on_device != 0);
     if (synchronize) check_numeric(p);
   });
@@ -1033,6 +1062,7 @@ int slsht_cuda_modulated(slsht_cuda_plan* p, const double* f, int count, const i
     CKL();
     std::vector<double2> hU((size_t)count * p->NPQ);
     CK(cudaMemcpyAsync(hU.data(), U, hU.size() * 16, cudaMemcpyDeviceToHost, s));
+    join_aux(p);
     CK(cudaStreamSynchronize(s));
     cudaFree(ds);
     cudaFree(dt);
