@@ -56,6 +56,17 @@ struct LnRows {
     return s;
   }
   static constexpr int UPAD = urows() + ((4 - urows()) % 8 + 8) % 8;
+  static constexpr int qoff(int jq) {
+    int s = 0;
+    for (int j = 0; j < jq; ++j) s += np(j);
+    return s;
+  }
+  static constexpr int urb(int jq) {  // start of q row jq's padded block in a U row
+    int s = 0;
+    for (int j = 0; j < jq; ++j) s += (np(j) + 3) / 4 * 4;
+    return s;
+  }
+  static constexpr int jq_of_row(int x) { return x <= L ? x + L : x - L - 1; }  // T row = q mod n
 };
 
 template <int N>
@@ -187,6 +198,45 @@ struct FftDifDigest {
   }
 };
 
+// DMMA chains of first-stage row group CW (T rows CW + k MP, k < R1): Gauss 3-product complex
+// MMA over the k-steps of each row's q block. Every row offset and k-step count is a
+// compile-time constant (the warp dispatches on its group once per tile), so the loop has no
+// guards and the operand addresses are immediates.
+template <int N, int CW>
+struct LnRowGroup {
+  using Cfg = LnCfg<N>;
+  using Rows = typename Cfg::Rows;
+  static constexpr int R1 = Cfg::R1, MP = Cfg::MP, NT = Cfg::NT;
+  __device__ __forceinline__ static void mma(int cw, const double2* Us, const double2* Ws,
+                                             int lane, double (&c1)[R1][2], double (&c2)[R1][2],
+                                             double (&c3)[R1][2]) {
+    if constexpr (CW + 1 < MP) {
+      if (cw != CW) {
+        LnRowGroup<N, CW + 1>::mma(cw, Us, Ws, lane, c1, c2, c3);
+        return;
+      }
+    }
+    const int kl = lane & 3, ar = lane >> 2;
+    const double2* Ua = Us + ar * Cfg::UPAD + kl;
+#pragma unroll
+    for (int k = 0; k < R1; ++k) c1[k][0] = c1[k][1] = c2[k][0] = c2[k][1] = c3[k][0] = c3[k][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < Cfg::KSMAX; ++ks)
+#pragma unroll
+      for (int k = 0; k < R1; ++k) {
+        const int jq = Rows::jq_of_row(CW + k * MP);
+        if (ks < (Rows::np(jq) + 3) / 4) {
+          const int wr = Rows::qoff(jq) + 4 * ks + kl;
+          const double2 a = Ua[Rows::urb(jq) + 4 * ks];
+          const double2 b = Ws[wr * NT + (ar ^ ((2 * wr) & 7))];
+          dmma(c1[k][0], c1[k][1], a.x + a.y, b.x);
+          dmma(c2[k][0], c2[k][1], a.x, b.y - b.x);
+          dmma(c3[k][0], c3[k][1], a.y, b.x + b.y);
+        }
+      }
+  }
+};
+
 template <int N>
 __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const LnParams LP) {
   using Cfg = LnCfg<N>;
@@ -266,16 +316,6 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
     const int cw = warp - 1;  // row group: T rows cw + k MP, k < R1 (one first-stage butterfly)
     const int c_tid = tid - 32;
     const int kl = lane & 3, ar = lane >> 2;
-    // per row of the group: its q row, k-steps, U and W offsets
-    int nks[R1], gr[R1], uo[R1];
-#pragma unroll
-    for (int k = 0; k < R1; ++k) {
-      const int x = cw + k * MP;                   // T row = q mod n
-      const int jq = x <= L ? x + L : x - L - 1;  // q + L
-      nks[k] = (L + 1 - abs(jq - L) + 3) >> 2;
-      gr[k] = qoff_s[jq];
-      uo[k] = ar * Cfg::UPAD + urb_s[jq] + kl;
-    }
     const int a0 = dif_last_freq0<N, Cfg::RLAST>(c_tid / (MT * NT));
     uint32_t uphase = 0;
     long long t = 0;  // global tile counter of this CTA
@@ -301,22 +341,8 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
         if (tr) LP.trace[t * 8 + 2] = clock64();
 #endif
         const double2* Ws = Wsb + sl * WE;
-        // R1 independent DMMA chains (Gauss 3-product complex MMA), fully unrolled over k-steps
         double c1[R1][2], c2[R1][2], c3[R1][2];
-#pragma unroll
-        for (int k = 0; k < R1; ++k) c1[k][0] = c1[k][1] = c2[k][0] = c2[k][1] = c3[k][0] = c3[k][1] = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < Cfg::KSMAX; ++ks)
-#pragma unroll
-          for (int k = 0; k < R1; ++k)
-            if (ks < nks[k]) {
-              const int wr = gr[k] + 4 * ks + kl;
-              const double2 a = Us[uo[k] + 4 * ks];
-              const double2 b = Ws[wr * NT + (ar ^ ((2 * wr) & 7))];
-              dmma(c1[k][0], c1[k][1], a.x + a.y, b.x);
-              dmma(c2[k][0], c2[k][1], a.x, b.y - b.x);
-              dmma(c3[k][0], c3[k][1], a.y, b.x + b.y);
-            }
+        LnRowGroup<N, 0>::mma(cw, Us, Ws, lane, c1, c2, c3);
 #ifdef SLSHT_WS_TRACE
         if (tr) LP.trace[t * 8 + 3] = clock64();
 #endif
