@@ -217,7 +217,9 @@ std::vector<int> factor_odd(int n) {
 // Tile shape of k_couple per transform length: the CTA keeps 8*MG x 8*NG x n complex of T in
 // shared memory (<= ~135 KB), DESIGN.md §3.3.
 void couple_tile(int n, int& MG, int& NG) {
-  MG = n <= 65 ? 2 : 1;
+  // n = 49, 65: one 8x8 tile per CTA so that 3 CTAs share an SM and overlap their coupling,
+  // FFT and store phases (a 16-component tile needs the whole shared memory)
+  MG = (n <= 33) ? 2 : 1;
   NG = n <= 31 ? 2 : 1;
 }
 
@@ -234,8 +236,8 @@ CoupleFn couple_kernel(int n, int MG, int NG) {
   switch (n) {
     case 17: return k_couple<17, 2, 2, 512, 1>;
     case 33: return k_couple<33, 2, 1, 256, 2>;
-    case 49: return k_couple<49, 2, 1, 512, 1>;
-    case 65: return k_couple<65, 2, 1, 512, 1>;
+    case 49: return k_couple<49, 1, 1, 256, 3>;
+    case 65: return k_couple<65, 1, 1, 256, 2>;
     case 129: return k_couple<129, 1, 1, 256, 1>;
     default: break;
   }
@@ -266,8 +268,6 @@ bool ws_kernel(int n, WsKernel& k) {
 int couple_threads(int n) {
   switch (n) {
     case 17:
-    case 49:
-    case 65:
       return 512;
     default:
       return 256;
