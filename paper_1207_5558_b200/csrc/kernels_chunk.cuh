@@ -45,9 +45,12 @@ __global__ void __launch_bounds__(128) k_agen(const Seg* __restrict__ segs, int 
 // tensor cores:
 //   mod[row][c] = sum_j A[row][j] * B_m[j][c],  B_m[j][c] = I(theta_j, m - q_c) lambda_c(theta_j)
 // (zero where |m - q_c| > L_f), c in q-major (p, q) order. U = conj(mod) is stored.
-// CTA tile 32 rows x 64 complex columns, K chunks of 32 nodes; B_m is generated on the fly
-// into shared memory and reused by the 32 rows. 8 warps = 2 row groups x 4 column groups,
-// each warp 16 rows x 16 complex columns = 8 DMMA per k-step of 4.
+// CTA tile 32 rows x 64 complex columns, K chunks of 32 nodes, 8 warps = 2 row groups x 4
+// column groups, each warp 16 rows x 16 complex columns = 8 DMMA per k-step of 4.
+// Operands stream through a two-stage cp.async pipeline: the A rows, the raw lambda_c rows
+// and the I values of the few distinct q of the column tile (B_m = I * lambda is formed at the
+// MMA, two multiplies per fragment). A, lambda and I rows have the padded node stride ldA
+// (zeros past n_nodes), so every copy is a whole 16-B chunk.
 struct MTile {
   int m, row0, rows;
 };
@@ -55,6 +58,25 @@ struct MTile {
 constexpr int MG_ROWS = 32;  // rows per CTA tile
 constexpr int MG_COLS = 64;  // complex columns per CTA tile
 constexpr int MG_K = 32;     // nodes per K chunk
+constexpr int MG_NQ = 16;    // distinct q per column tile (host-checked)
+constexpr int MG_KS = MG_K + 4;  // padded row stride of the A and lambda stages (doubles)
+constexpr size_t MG_STAGE = (size_t)MG_ROWS * MG_KS * 8 + (size_t)MG_COLS * MG_KS * 8 +
+                            (size_t)MG_K * MG_NQ * 16;
+constexpr size_t MG_SMEM = 2 * MG_STAGE;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(pred ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory");
+}
 
 __global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles, int n_nodes,
                                                  int ldA, int L_f, int NPQ,
@@ -66,15 +88,48 @@ __global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles
                                                  const int* __restrict__ u_base,
                                                  const int* __restrict__ u_str,
                                                  double2* __restrict__ U) {
-  __shared__ double As[MG_ROWS][MG_K + 4];
-  __shared__ double Br[MG_K][MG_COLS + 4];
-  __shared__ double Bi[MG_K][MG_COLS + 4];
+  extern __shared__ __align__(16) unsigned char mg_smem[];
   __shared__ int colq[MG_COLS];
   const MTile t = tiles[blockIdx.x];
   const int cbase = blockIdx.y * MG_COLS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rg = warp >> 2, cgp = warp & 3;
+  // a warp whose 16 columns all lie past NPQ (last column tile) has no MMA work
+  const bool warp_cols = cbase + cgp * 16 < NPQ;
   if (tid < MG_COLS) colq[tid] = (cbase + tid < NPQ) ? pq_q[2 * (cbase + tid)] : 0;
+  __syncthreads();
+  const int q_lo = colq[0];
+  const int nq = colq[min(MG_COLS, NPQ - cbase) - 1] - q_lo + 1;
+  auto stage_a = [&](int b) { return reinterpret_cast<double*>(mg_smem + b * MG_STAGE); };
+  auto stage_l = [&](int b) { return stage_a(b) + MG_ROWS * MG_KS; };
+  auto stage_i = [&](int b) {
+    return reinterpret_cast<double2*>(stage_l(b) + MG_COLS * MG_KS);
+  };
+  auto issue = [&](int k0, int b) {
+    double* As = stage_a(b);
+    double* Ls = stage_l(b);
+    double2* Is = stage_i(b);
+#pragma unroll
+    for (int i = 0; i < MG_ROWS * MG_K / 2 / 256; ++i) {
+      const int e = tid + 256 * i, r = e / (MG_K / 2), u = e % (MG_K / 2);
+      const bool ok = r < t.rows;
+      cp_async16(As + r * MG_KS + 2 * u, A + (size_t)(t.row0 + (ok ? r : 0)) * ldA + k0 + 2 * u, ok);
+    }
+#pragma unroll
+    for (int i = 0; i < MG_COLS * MG_K / 2 / 256; ++i) {
+      const int e = tid + 256 * i, cc = e / (MG_K / 2), u = e % (MG_K / 2);
+      const bool ok = cbase + cc < NPQ;
+      cp_async16(Ls + cc * MG_KS + 2 * u, lamh + (size_t)(ok ? cbase + cc : 0) * ldA + k0 + 2 * u, ok);
+    }
+#pragma unroll
+    for (int i = 0; i < MG_K * MG_NQ / 256; ++i) {
+      const int e = tid + 256 * i, k = e % MG_K, sq = e / MG_K;
+      const int mu = t.m - (q_lo + sq);
+      const bool ok = sq < nq && mu >= -L_f && mu <= L_f;
+      cp_async16(Is + k * MG_NQ + sq, itab + (size_t)(ok ? mu + L_f : 0) * ldA + k0 + k, ok);
+    }
+    cp_async_commit();
+  };
   double acc[2][2][2][2];  // [row frag][col frag][re/im][e]
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -82,50 +137,47 @@ __global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles
     for (int b = 0; b < 2; ++b)
 #pragma unroll
       for (int c = 0; c < 2; ++c) acc[a][b][c][0] = acc[a][b][c][1] = 0.0;
-  __syncthreads();
-  const int kk = tid & 31;  // node within the chunk handled by this thread in the B build
-  for (int k0 = 0; k0 < ldA; k0 += MG_K) {
+  int qi[2];
 #pragma unroll
-    for (int it = 0; it < MG_ROWS * MG_K / 256; ++it) {
-      const int e = tid + it * 256;
-      const int r = e / MG_K, k = e % MG_K;
-      As[r][k] = (r < t.rows) ? A[(size_t)(t.row0 + r) * ldA + k0 + k] : 0.0;
+  for (int cf = 0; cf < 2; ++cf) qi[cf] = colq[cgp * 16 + cf * 8 + (lane >> 2)] - q_lo;
+  const int nchunks = ldA / MG_K;
+  issue(0, 0);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int k0 = ch * MG_K;
+    if (ch + 1 < nchunks) {
+      issue(k0 + MG_K, (ch + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-    const int j = k0 + kk;
+    __syncthreads();
+    const double* As = stage_a(ch & 1);
+    const double* Ls = stage_l(ch & 1);
+    const double2* Is = stage_i(ch & 1);
+    // k-steps holding at least one node (the last chunk is mostly padding)
+    const int ksn = min(MG_K / 4, (n_nodes - k0 + 3) / 4);
+    if (warp_cols) {
 #pragma unroll
-    for (int it = 0; it < MG_COLS / 8; ++it) {
-      const int cc = (tid >> 5) + 8 * it;
-      const int c = cbase + cc;
-      double vr = 0.0, vi = 0.0;
-      if (c < NPQ && j < n_nodes) {
-        const int mu = t.m - colq[cc];
-        if (mu >= -L_f && mu <= L_f) {
-          const double2 iv = itab[(size_t)(mu + L_f) * n_nodes + j];
-          const double lv = lamh[(size_t)c * n_nodes + j];
-          vr = iv.x * lv;
-          vi = iv.y * lv;
+      for (int ks = 0; ks < MG_K / 4; ++ks) {
+        if (ks < ksn) {
+          const int k = ks * 4 + (lane & 3);
+          const double a0 = As[(rg * 16 + (lane >> 2)) * MG_KS + k];
+          const double a1 = As[(rg * 16 + 8 + (lane >> 2)) * MG_KS + k];
+#pragma unroll
+          for (int cf = 0; cf < 2; ++cf) {
+            const int col = cgp * 16 + cf * 8 + (lane >> 2);
+            const double lv = Ls[col * MG_KS + k];
+            const double2 iv = Is[k * MG_NQ + qi[cf]];
+            const double br = iv.x * lv, bi = iv.y * lv;
+            dmma(acc[0][cf][0][0], acc[0][cf][0][1], a0, br);
+            dmma(acc[0][cf][1][0], acc[0][cf][1][1], a0, bi);
+            dmma(acc[1][cf][0][0], acc[1][cf][0][1], a1, br);
+            dmma(acc[1][cf][1][0], acc[1][cf][1][1], a1, bi);
+          }
         }
       }
-      Br[kk][cc] = vr;
-      Bi[kk][cc] = vi;
     }
-    __syncthreads();
-#pragma unroll
-    for (int ks = 0; ks < MG_K / 4; ++ks) {
-      const int k = ks * 4 + (lane & 3);
-      const double a0 = As[rg * 16 + (lane >> 2)][k];
-      const double a1 = As[rg * 16 + 8 + (lane >> 2)][k];
-#pragma unroll
-      for (int cf = 0; cf < 2; ++cf) {
-        const int col = cgp * 16 + cf * 8 + (lane >> 2);
-        const double br = Br[k][col], bi = Bi[k][col];
-        dmma(acc[0][cf][0][0], acc[0][cf][0][1], a0, br);
-        dmma(acc[0][cf][1][0], acc[0][cf][1][1], a0, bi);
-        dmma(acc[1][cf][0][0], acc[1][cf][0][1], a1, br);
-        dmma(acc[1][cf][1][0], acc[1][cf][1][1], a1, bi);
-      }
-    }
-    __syncthreads();
+    __syncthreads();  // stage ch & 1 is refilled by the issue of chunk ch + 2
   }
 #pragma unroll
   for (int rf = 0; rf < 2; ++rf) {

@@ -67,9 +67,10 @@ __global__ void k_nodes(int N, double* __restrict__ ncos, double* __restrict__ n
   }
 }
 
-// lambda_p^q(theta_j) for the window band, rows in q-major (p, q) order: row c = qoff[q+L] + p-|q|.
+// lambda_p^q(theta_j) for the window band, rows in q-major (p, q) order: row c = qoff[q+L] + p-|q|,
+// row stride ld (>= n_nodes; the padding stays zero).
 // grid (node blocks, 2L_h+1 orders); dynamic smem 3 (L_h+1) doubles.
-__global__ void k_legendre_window(int L_h, int n_nodes, const double* __restrict__ ncos,
+__global__ void k_legendre_window(int L_h, int n_nodes, int ld, const double* __restrict__ ncos,
                                   const double* __restrict__ nsin, const int* __restrict__ qoff,
                                   double* __restrict__ lamh) {
   extern __shared__ double coef[];
@@ -85,13 +86,13 @@ __global__ void k_legendre_window(int L_h, int n_nodes, const double* __restrict
   const int base = qoff[q + L_h];
   for (int p = aq; p <= L_h; ++p) {
     if (p > aq) r.next(ca, cb);
-    lamh[(size_t)(base + p - aq) * n_nodes + j] = r.cur;
+    lamh[(size_t)(base + p - aq) * ld + j] = r.cur;
   }
 }
 
 // I(theta_j, mu) = 2 pi conj(sum_{l=|mu|}^{L_f} f_l^mu lambda_l^mu(theta_j)) (transform.cpp:158-173)
 // grid (node blocks, 2L_f+1 orders); dynamic smem 3 (L_f+1) doubles + (L_f+1) complex (f_l^mu).
-__global__ void k_itab(int L_f, int n_nodes, const double* __restrict__ ncos,
+__global__ void k_itab(int L_f, int n_nodes, int ld, const double* __restrict__ ncos,
                        const double* __restrict__ nsin, const double* __restrict__ f,
                        double* __restrict__ itab) {
   extern __shared__ double coef[];
@@ -117,7 +118,7 @@ __global__ void k_itab(int L_f, int n_nodes, const double* __restrict__ ncos,
   double2 o;
   o.x = 2.0 * kPi * ar;
   o.y = -(2.0 * kPi * ai);
-  reinterpret_cast<double2*>(itab)[(size_t)(mu + L_f) * n_nodes + j] = o;
+  reinterpret_cast<double2*>(itab)[(size_t)(mu + L_f) * ld + j] = o;
 }
 
 // Delta^p = d^p(pi/2) for p <= L (wigner.cpp:28-80), one CTA, level by level. The previous

@@ -526,8 +526,11 @@ void build_plan(slsht_cuda_plan* p) {
   p->d_nsin = dalloc<double>(p->n_nodes);
   p->d_weights = dalloc<double>(p->n_nodes);
   p->d_betaw = dalloc<double>(p->nb);
-  p->d_itab = dalloc<double2>((size_t)(2 * Lf + 1) * p->n_nodes);
-  p->d_lamh = dalloc<double>((size_t)p->NPQ * p->n_nodes);
+  // node stride ldA (a multiple of the modulated-SHT K chunk), padding zero for the 16-B copies
+  p->d_itab = dalloc<double2>((size_t)(2 * Lf + 1) * p->ldA);
+  p->d_lamh = dalloc<double>((size_t)p->NPQ * p->ldA);
+  CK(cudaMemsetAsync(p->d_itab, 0, sizeof(double2) * (2 * Lf + 1) * p->ldA, s));
+  CK(cudaMemsetAsync(p->d_lamh, 0, sizeof(double) * p->NPQ * p->ldA, s));
   size_t dsz = 0;
   for (int pp = 0; pp <= L; ++pp) dsz += (size_t)(2 * pp + 1) * (2 * pp + 1);
   p->d_delta = dalloc<double>(dsz);
@@ -574,6 +577,12 @@ void build_plan(slsht_cuda_plan* p) {
   for (auto& e : p->ev_stage) CK(cudaEventCreate(&e));
 
   p->num_sms = prop.multiProcessorCount;
+  CK(cudaFuncSetAttribute(k_modgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM));
+  for (int c0 = 0; c0 < p->NPQ; c0 += MG_COLS) {  // distinct q per modulated-SHT column tile
+    const int c1 = std::min(p->NPQ, c0 + MG_COLS) - 1;
+    if (pq[2 * c1] - pq[2 * c0] + 1 > MG_NQ)
+      throw Status{SLSHT_ERR_VALIDATION, "internal: column tile spans too many orders q"};
+  }
   if (p->use_lines) {
     CK(cudaFuncSetAttribute(p->lines_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)p->couple_smem));
@@ -624,11 +633,11 @@ void run_setup(slsht_cuda_plan* p) {
                                                        L, p->d_betaw, p->d_err);  // warp per weight
   CKL();
   k_legendre_window<<<dim3((p->n_nodes + 127) / 128, p->n), 128, 3 * (L + 1) * sizeof(double), s>>>(
-      L, p->n_nodes, p->d_ncos, p->d_nsin, p->d_qoff, p->d_lamh);
+      L, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_qoff, p->d_lamh);
   CKL();
   k_itab<<<dim3((p->n_nodes + 127) / 128, 2 * p->L_f + 1), 128,
            (5 * (p->L_f + 1) + 1) * sizeof(double), s>>>(
-      p->L_f, p->n_nodes, p->d_ncos, p->d_nsin, p->d_f, reinterpret_cast<double*>(p->d_itab));
+      p->L_f, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_f, reinterpret_cast<double*>(p->d_itab));
   CKL();
   cudaStream_t a = p->aux_stream;
   CK(launch_delta(L, p->d_delta, a));
@@ -655,7 +664,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
       p->d_segs + ch.seg0, p->L_g, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_weights, p->d_A);
   CKL();
   record(p, 1);
-  k_modgemm<<<dim3(ch.ntile, (p->NPQ + MG_COLS - 1) / MG_COLS), 256, 0, s>>>(
+  k_modgemm<<<dim3(ch.ntile, (p->NPQ + MG_COLS - 1) / MG_COLS), 256, MG_SMEM, s>>>(
       p->d_tiles + ch.tile0, p->n_nodes, p->ldA, p->L_f, p->NPQ, p->d_A, p->d_itab, p->d_lamh,
       p->d_pq, p->use_lines ? 8 : (p->use_ws ? p->ws.MT : 0), p->ws_stages.group_elems,
       p->d_ubase, p->d_ustr, p->d_U);
@@ -1056,7 +1065,7 @@ int slsht_cuda_modulated(slsht_cuda_plan* p, const double* f, int count, const i
     k_agen<<<dim3(count, (p->ldA + 127) / 128), 128, 3 * (p->L_g + 1) * sizeof(double), s>>>(
         ds, p->L_g, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_weights, A);
     CKL();
-    k_modgemm<<<dim3(count, (p->NPQ + MG_COLS - 1) / MG_COLS), 256, 0, s>>>(
+    k_modgemm<<<dim3(count, (p->NPQ + MG_COLS - 1) / MG_COLS), 256, MG_SMEM, s>>>(
         dt, p->n_nodes, p->ldA, p->L_f, p->NPQ, A, p->d_itab, p->d_lamh, p->d_pq, 0, 0, nullptr,
         nullptr, U);
     CKL();
