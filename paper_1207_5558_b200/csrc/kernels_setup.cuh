@@ -121,120 +121,127 @@ __global__ void k_itab(int L_f, int n_nodes, int ld, const double* __restrict__ 
   reinterpret_cast<double2*>(itab)[(size_t)(mu + L_f) * ld + j] = o;
 }
 
-// Delta^p = d^p(pi/2) for p <= L (wigner.cpp:28-80), one CTA, level by level. The previous
-// level's top row is staged in shared memory; each level's non-negative sector is built in
-// shared memory (downward three-term recursion per column, then transpose) and written to
-// global through the d-matrix symmetries. Explicit _rn intrinsics keep every operation
-// separately rounded (no FMA contraction), so the table is bit-identical to the reference.
-// PRE: the recursion coefficients of a level (a square root and a division per (m, m') --
-// the slow part) are computed by all threads before the recursion, so the serial chain of a
-// column is two multiplies and a subtraction per step. Shared memory: 2 S^2 + 2 S doubles
-// (PRE) or S^2 + S, S = L + 1.
-template <bool PRE>
-__global__ void k_delta(int L, double* __restrict__ delta) {
-  extern __shared__ double sm[];
-  const int S = L + 1;
-  double* sec = sm;           // S x S sector [m][mp], m, mp >= 0
-  double* top = sm + S * S;   // previous level's top row Delta^{l-1}_{l-1, mp}
-  double* ca = top + S;       // PRE: 2 mp / sqrt((l - m)(l + m + 1)) at [m][mp]
-  double* cc = ca + S * S;    // PRE: sqrt((l - m - 1)(l + m + 2)) / sqrt((l - m)(l + m + 1))
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    delta[0] = 1.0;
-    top[0] = 1.0;
+__device__ __forceinline__ size_t delta_offset(int p) {
+  return (size_t)p * (2 * p - 1) * (2 * p + 1) / 3;
+}
+
+// Delta^p = d^p(pi/2) for p <= L (wigner.cpp:28-80). The reference builds level l from level
+// l-1 only through its top row, so the levels decouple once the top rows are known:
+//   1. every top-row factor (a square root and a division each) in parallel;
+//   2. the top rows: Delta^l_{l,0} chains down the levels, then Delta^l_{l,m'} for m' >= 1
+//      chains along the diagonal l - m' (one multiply per step);
+//   3. every column (l, m') of every level's m >= m' sector in parallel: the downward
+//      three-term recursion in m with the values in registers, each value written straight to
+//      all its symmetric positions (transpose with (-1)^(m-m'), then the four quadrants).
+// Explicit _rn intrinsics keep every operation of the reference separately rounded (no FMA
+// contraction), so the table is bit-identical to the reference. One CTA; shared memory
+// (L+1)(L+2) doubles.
+__device__ __forceinline__ int tri_index(int l, int mp) { return l * (l + 1) / 2 + mp; }
+
+__device__ __forceinline__ void delta_put(double* lev, int l, int m, int mp, double v) {
+  // v = sector value at (m, mp), m >= mp >= 0 (and its transpose when m != mp)
+  const int w = 2 * l + 1;
+#pragma unroll
+  for (int tr = 0; tr < 2; ++tr) {
+    if (tr == 1 && m == mp) break;
+    const int a = tr ? mp : m, b = tr ? m : mp;  // sector position (a, b)
+    const double sv = tr ? (((m - mp) & 1) ? -1.0 : 1.0) * v : v;
+#pragma unroll
+    for (int sq = 0; sq < 2; ++sq) {
+      if (sq == 1 && a == 0) break;
+      const int q = sq ? -a : a;
+#pragma unroll
+      for (int sqp = 0; sqp < 2; ++sqp) {
+        if (sqp == 1 && b == 0) break;
+        const int qp = sqp ? -b : b;
+        double sgn = 1.0;
+        if (q < 0 && qp >= 0) sgn = ((l + b) & 1) ? -1.0 : 1.0;
+        else if (q >= 0 && qp < 0) sgn = ((l + a) & 1) ? -1.0 : 1.0;
+        else if (q < 0 && qp < 0) sgn = ((a + b) & 1) ? -1.0 : 1.0;
+        lev[(q + l) * w + qp + l] = sgn * sv;
+      }
+    }
   }
-  __syncthreads();
-  size_t off = 1;
-  for (int l = 1; l <= L; ++l) {
-    const int w = 2 * l + 1;
-    // top row m = l from the previous degree (Trapani seeds)
-    for (int mp = tid; mp <= l; mp += blockDim.x) {
-      double v;
+}
+
+__global__ void __launch_bounds__(1024) k_delta(int L, double* __restrict__ delta) {
+  extern __shared__ double sm[];
+  const int T = (L + 1) * (L + 2) / 2;
+  double* fac = sm;      // [tri(l, mp)] top-row factor of level l
+  double* top = sm + T;  // [tri(l, mp)] Delta^l_{l, mp}
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < T; i += nt) {
+    int l = (int)((sqrt(8.0 * i + 1.0) - 1.0) * 0.5);
+    while (tri_index(l + 1, 0) <= i) ++l;
+    while (tri_index(l, 0) > i) --l;
+    const int mp = i - tri_index(l, 0);
+    double f = 1.0;
+    if (l > 0) {
       if (mp == 0) {
-        v = __dmul_rn(-__dsqrt_rn(__ddiv_rn(2.0 * l - 1.0, 2.0 * l)), top[0]);
+        f = -__dsqrt_rn(__ddiv_rn(2.0 * l - 1.0, 2.0 * l));
       } else {
         const double num = __dmul_rn((double)l, 2.0 * l - 1.0);
         const double den = __dmul_rn(2.0 * (l + mp), (double)l + mp - 1.0);
-        v = __dmul_rn(__dsqrt_rn(__ddiv_rn(num, den)), top[mp - 1]);
-      }
-      sec[l * S + mp] = v;
-    }
-    if constexpr (PRE) {
-      for (int idx = tid; idx < l * l; idx += blockDim.x) {
-        const int m = idx / l, mp = idx % l;
-        if (mp > m) continue;
-        const double denom = __dsqrt_rn(__dmul_rn((double)(l - m), l + m + 1.0));
-        ca[m * S + mp] = __ddiv_rn(2.0 * mp, denom);
-        if (mp == 0 && m + 2 <= l)
-          cc[m] = __ddiv_rn(__dsqrt_rn(__dmul_rn(l - m - 1.0, l + m + 2.0)), denom);
+        f = __dsqrt_rn(__ddiv_rn(num, den));
       }
     }
-    __syncthreads();
-    // downward recursion in m over the sector m >= mp >= 0, one column per thread
-    for (int mp = tid; mp <= l - 1; mp += blockDim.x) {
-      for (int m = l - 1; m >= mp; --m) {
-        double value;
-        if constexpr (PRE) {
-          value = __dmul_rn(ca[m * S + mp], sec[(m + 1) * S + mp]);
-          if (m + 2 <= l) value = __dsub_rn(value, __dmul_rn(cc[m], sec[(m + 2) * S + mp]));
-        } else {
-          const double denom = __dsqrt_rn(__dmul_rn((double)(l - m), l + m + 1.0));
-          value = __dmul_rn(__ddiv_rn(2.0 * mp, denom), sec[(m + 1) * S + mp]);
-          if (m + 2 <= l) {
-            const double c2 = __ddiv_rn(__dsqrt_rn(__dmul_rn(l - m - 1.0, l + m + 2.0)), denom);
-            value = __dsub_rn(value, __dmul_rn(c2, sec[(m + 2) * S + mp]));
-          }
-        }
-        sec[m * S + mp] = value;
+    fac[i] = f;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double v = 1.0;
+    top[0] = 1.0;
+    for (int l = 1; l <= L; ++l) {
+      v = __dmul_rn(fac[tri_index(l, 0)], v);
+      top[tri_index(l, 0)] = v;
+    }
+  }
+  __syncthreads();
+  for (int d = tid; d < L; d += nt) {  // diagonal l - mp = d, mp >= 1
+    double v = top[tri_index(d, 0)];
+    for (int mp = 1; d + mp <= L; ++mp) {
+      const int l = d + mp;
+      v = __dmul_rn(fac[tri_index(l, mp)], v);
+      top[tri_index(l, mp)] = v;
+    }
+  }
+  __syncthreads();
+  // columns: item = tri(l, mp) over all levels (top-row entries included)
+  for (int i = tid; i < T; i += nt) {
+    int l = (int)((sqrt(8.0 * i + 1.0) - 1.0) * 0.5);
+    while (tri_index(l + 1, 0) <= i) ++l;
+    while (tri_index(l, 0) > i) --l;
+    const int mp = i - tri_index(l, 0);
+    double* lev = delta + delta_offset(l);
+    double v1 = top[i];  // (m + 1, mp) as m runs down; starts at m = l
+    delta_put(lev, l, l, mp, v1);
+    double v2 = 0.0;     // (m + 2, mp)
+    for (int m = l - 1; m >= mp; --m) {
+      const double denom = __dsqrt_rn(__dmul_rn((double)(l - m), l + m + 1.0));
+      double value = __dmul_rn(__ddiv_rn(2.0 * mp, denom), v1);
+      if (m + 2 <= l) {
+        const double c2 = __ddiv_rn(__dsqrt_rn(__dmul_rn(l - m - 1.0, l + m + 2.0)), denom);
+        value = __dsub_rn(value, __dmul_rn(c2, v2));
       }
+      delta_put(lev, l, m, mp, value);
+      v2 = v1;
+      v1 = value;
     }
-    __syncthreads();
-    // transpose into the upper triangle
-    for (int idx = tid; idx < (l + 1) * (l + 1); idx += blockDim.x) {
-      const int m = idx / (l + 1), mp = idx % (l + 1);
-      if (mp > m) sec[m * S + mp] = (((mp - m) & 1) ? -1.0 : 1.0) * sec[mp * S + m];
-    }
-    __syncthreads();
-    // write the full level through the symmetries
-    double* lev = delta + off;
-    for (int idx = tid; idx < w * w; idx += blockDim.x) {
-      const int q = idx / w - l, qp = idx % w - l;
-      const int m = q < 0 ? -q : q, mp = qp < 0 ? -qp : qp;
-      const double v = sec[m * S + mp];
-      double sgn = 1.0;
-      if (q < 0 && qp >= 0) sgn = ((l + mp) & 1) ? -1.0 : 1.0;
-      else if (q >= 0 && qp < 0) sgn = ((l + m) & 1) ? -1.0 : 1.0;
-      else if (q < 0 && qp < 0) sgn = ((m + mp) & 1) ? -1.0 : 1.0;
-      lev[idx] = sgn * v;
-    }
-    for (int mp = tid; mp <= l; mp += blockDim.x) top[mp] = sec[l * S + mp];
-    off += (size_t)w * w;
-    __syncthreads();
   }
 }
 
 // Launch k_delta for band limit L on stream s (one CTA).
 inline cudaError_t launch_delta(int L, double* out, cudaStream_t s) {
-  const size_t S = (size_t)L + 1;
-  const size_t pre = sizeof(double) * (2 * S * S + 2 * S), plain = sizeof(double) * (S * S + S);
-  if (pre <= 227 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_delta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)pre);
-    if (e != cudaSuccess) return e;
-    k_delta<true><<<1, 256, pre, s>>>(L, out);
-  } else {
-    if (plain > 227 * 1024) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(k_delta<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plain);
-    if (e != cudaSuccess) return e;
-    k_delta<false><<<1, 256, plain, s>>>(L, out);
-  }
+  const size_t T = (size_t)(L + 1) * (L + 2) / 2;
+  const size_t bytes = sizeof(double) * 2 * T;
+  if (bytes > 227 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k_delta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)bytes);
+  if (e != cudaSuccess) return e;
+  k_delta<<<1, 1024, bytes, s>>>(L, out);
   return cudaGetLastError();
 }
 
-__device__ __forceinline__ size_t delta_offset(int p) {
-  return (size_t)p * (2 * p - 1) * (2 * p + 1) / 3;
-}
 
 // d^p_{q,q'}(beta_b) = Re[i^{q-q'} sum_q'' Delta^p_{q''q} Delta^p_{q''q'} e^{-i q'' beta_b}]
 // (wigner.hpp:55-60), beta_b = 2 pi b / n for b <= L. Layout [p][q][q'][b].

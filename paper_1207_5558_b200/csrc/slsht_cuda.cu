@@ -1026,7 +1026,7 @@ int slsht_cuda_delta_tables(int device, int L, double* out) {
     size_t dsz = 0;
     for (int pp = 0; pp <= L; ++pp) dsz += (size_t)(2 * pp + 1) * (2 * pp + 1);
     double* d = dalloc<double>(dsz);
-    if ((size_t)(L + 1) * (L + 1) * 8 > 220 * 1024)
+    if ((size_t)(L + 1) * (L + 2) * 8 > 227 * 1024)
       throw Status{SLSHT_ERR_VALIDATION, "band limit too large for the on-chip Delta recursion"};
     CK(launch_delta(L, d, 0));
     CK(cudaMemcpy(out, d, dsz * sizeof(double), cudaMemcpyDeviceToHost));
