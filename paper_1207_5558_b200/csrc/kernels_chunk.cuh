@@ -78,26 +78,24 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory");
 }
 
-__global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles, int n_nodes,
-                                                 int ldA, int L_f, int NPQ,
-                                                 const double* __restrict__ A,
-                                                 const double2* __restrict__ itab,
-                                                 const double* __restrict__ lamh,
-                                                 const int* __restrict__ pq_q,
-                                                 int u_group, long long u_gs,
-                                                 const int* __restrict__ u_base,
-                                                 const int* __restrict__ u_str,
-                                                 double2* __restrict__ U) {
+template <int RG>
+__device__ __forceinline__ void modgemm_tile(const MTile t, int n_nodes, int ldA, int L_f,
+                                             int NPQ, const int* colq,
+                                             const double* __restrict__ A,
+                                             const double2* __restrict__ itab,
+                                             const double* __restrict__ lamh, int u_group,
+                                             long long u_gs, const int* __restrict__ u_base,
+                                             const int* __restrict__ u_str,
+                                             double2* __restrict__ U) {
+  // RG row groups of 16 rows; the 8 warps split as RG x (8 / RG), each warp 16 rows x
+  // 8 RG complex columns (CF = RG column fragments)
+  constexpr int CF = RG, WPR = 8 / RG;
   extern __shared__ __align__(16) unsigned char mg_smem[];
-  __shared__ int colq[MG_COLS];
-  const MTile t = tiles[blockIdx.x];
   const int cbase = blockIdx.y * MG_COLS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rg = warp >> 2, cgp = warp & 3;
-  // a warp whose 16 columns all lie past NPQ (last column tile) has no MMA work
-  const bool warp_cols = cbase + cgp * 16 < NPQ;
-  if (tid < MG_COLS) colq[tid] = (cbase + tid < NPQ) ? pq_q[2 * (cbase + tid)] : 0;
-  __syncthreads();
+  const int rg = warp / WPR, cgp = warp % WPR;
+  // a warp whose columns all lie past NPQ (last column tile) has no MMA work
+  const bool warp_cols = cbase + cgp * 8 * CF < NPQ;
   const int q_lo = colq[0];
   const int nq = colq[min(MG_COLS, NPQ - cbase) - 1] - q_lo + 1;
   auto stage_a = [&](int b) { return reinterpret_cast<double*>(mg_smem + b * MG_STAGE); };
@@ -110,7 +108,7 @@ __global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles
     double* Ls = stage_l(b);
     double2* Is = stage_i(b);
 #pragma unroll
-    for (int i = 0; i < MG_ROWS * MG_K / 2 / 256; ++i) {
+    for (int i = 0; i < 16 * RG * MG_K / 2 / 256; ++i) {
       const int e = tid + 256 * i, r = e / (MG_K / 2), u = e % (MG_K / 2);
       const bool ok = r < t.rows;
       cp_async16(As + r * MG_KS + 2 * u, A + (size_t)(t.row0 + (ok ? r : 0)) * ldA + k0 + 2 * u, ok);
@@ -130,16 +128,16 @@ __global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles
     }
     cp_async_commit();
   };
-  double acc[2][2][2][2];  // [row frag][col frag][re/im][e]
+  double acc[2][CF][2][2];  // [row frag][col frag][re/im][e]
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < CF; ++b)
 #pragma unroll
       for (int c = 0; c < 2; ++c) acc[a][b][c][0] = acc[a][b][c][1] = 0.0;
-  int qi[2];
+  int qi[CF];
 #pragma unroll
-  for (int cf = 0; cf < 2; ++cf) qi[cf] = colq[cgp * 16 + cf * 8 + (lane >> 2)] - q_lo;
+  for (int cf = 0; cf < CF; ++cf) qi[cf] = colq[cgp * 8 * CF + cf * 8 + (lane >> 2)] - q_lo;
   const int nchunks = ldA / MG_K;
   issue(0, 0);
   for (int ch = 0; ch < nchunks; ++ch) {
@@ -164,8 +162,8 @@ __global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles
           const double a0 = As[(rg * 16 + (lane >> 2)) * MG_KS + k];
           const double a1 = As[(rg * 16 + 8 + (lane >> 2)) * MG_KS + k];
 #pragma unroll
-          for (int cf = 0; cf < 2; ++cf) {
-            const int col = cgp * 16 + cf * 8 + (lane >> 2);
+          for (int cf = 0; cf < CF; ++cf) {
+            const int col = cgp * 8 * CF + cf * 8 + (lane >> 2);
             const double lv = Ls[col * MG_KS + k];
             const double2 iv = Is[k * MG_NQ + qi[cf]];
             const double br = iv.x * lv, bi = iv.y * lv;
@@ -184,10 +182,10 @@ __global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles
     const int r = rg * 16 + rf * 8 + (lane >> 2);
     if (r >= t.rows) continue;
 #pragma unroll
-    for (int cf = 0; cf < 2; ++cf)
+    for (int cf = 0; cf < CF; ++cf)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int c = cbase + cgp * 16 + cf * 8 + 2 * (lane & 3) + e;
+        const int c = cbase + cgp * 8 * CF + cf * 8 + 2 * (lane & 3) + e;
         if (c < NPQ) {
           const int row = t.row0 + r;
           // u_group == 0: U[row][c]; else the stage-tiled layout of the warp-specialized
@@ -199,6 +197,30 @@ __global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles
         }
       }
   }
+}
+
+// Tiles of at most 16 rows (short order segments: the high-degree shards, the tail of every
+// order) take the 16-row variant; the others 32 rows.
+__global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles, int n_nodes,
+                                                 int ldA, int L_f, int NPQ,
+                                                 const double* __restrict__ A,
+                                                 const double2* __restrict__ itab,
+                                                 const double* __restrict__ lamh,
+                                                 const int* __restrict__ pq_q,
+                                                 int u_group, long long u_gs,
+                                                 const int* __restrict__ u_base,
+                                                 const int* __restrict__ u_str,
+                                                 double2* __restrict__ U) {
+  __shared__ int colq[MG_COLS];
+  const int cbase = blockIdx.y * MG_COLS;
+  if (threadIdx.x < MG_COLS)
+    colq[threadIdx.x] = (cbase + (int)threadIdx.x < NPQ) ? pq_q[2 * (cbase + threadIdx.x)] : 0;
+  __syncthreads();
+  const MTile t = tiles[blockIdx.x];
+  if (t.rows <= 16)
+    modgemm_tile<1>(t, n_nodes, ldA, L_f, NPQ, colq, A, itab, lamh, u_group, u_gs, u_base, u_str, U);
+  else
+    modgemm_tile<2>(t, n_nodes, ldA, L_f, NPQ, colq, A, itab, lamh, u_group, u_gs, u_base, u_str, U);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -37,7 +37,8 @@ struct LnParams {
   long long group_elems;  // U elements per group: MT rows of UPAD (zero-padded q blocks)
   int urb[136];           // per q row jq: offset of its padded row block in a U row
   int n_groups;
-  double* digest;         // [coeff_count(lmax)][8], rows coeff_index(l, m) (and the mirror)
+  int nseg;               // column segments per group: a work unit is (group, segment)
+  double* partials;       // [component][segment][8] digest partials (k_digest reduces them)
   long long* trace;       // debug (SLSHT_WS_TRACE builds)
 };
 
@@ -288,18 +289,26 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
   }
   __syncthreads();
 
+  // work units: (group g, column segment sg) storing tiles [seg_lo(sg), seg_lo(sg + 1)). A
+  // unit after the first also computes the tile before its range (no stores, no digest), so
+  // its first lines have their previous tile: every line is written whole by one unit.
+  const int n_units = LP.n_groups * LP.nseg;
+  auto seg_lo = [&](int sg) { return (int)(((long long)sg * nct) / LP.nseg); };
+  auto seg_c0 = [&](int sg) { return sg > 0 ? seg_lo(sg) - 1 : 0; };
+
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
     if (lane == 0) {
       uint32_t uphase = 0;
       long long t = 0;
-      for (int g = blockIdx.x; g < LP.n_groups; g += gridDim.x) {
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int g = u / LP.nseg, sg = u % LP.nseg;
         mbar_wait(uempty, uphase ^ 1);
         const uint32_t ub = (uint32_t)(LP.group_elems * 16);
         mbar_arrive_expect_tx(ufull, ub);
         bulk_g2s(Us, P.U + (size_t)g * LP.group_elems, ub, ufull);
         uphase ^= 1;
-        for (int ct = 0; ct < nct; ++ct, ++t) {
+        for (int ct = seg_c0(sg); ct < seg_lo(sg + 1); ++ct, ++t) {
           const int sl = (int)(t & 1);
           mbar_wait(&wempty[sl], (uint32_t)(((t >> 1) & 1) ^ 1));
           constexpr uint32_t wb = (uint32_t)(NPQ * NT * 16);
@@ -319,12 +328,14 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
     const int a0 = dif_last_freq0<N, Cfg::RLAST>(c_tid / (MT * NT));
     uint32_t uphase = 0;
     long long t = 0;  // global tile counter of this CTA
-    for (int g = blockIdx.x; g < LP.n_groups; g += gridDim.x) {
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const int g = u / LP.nseg, sg = u % LP.nseg;
+      const int s0 = seg_lo(sg), s1 = seg_lo(sg + 1);
       const int ncomp = min(MT, P.count - g * MT);
       DigestAcc D{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0};
       mbar_wait(ufull, uphase);
       uphase ^= 1;
-      for (int ct = 0; ct < nct; ++ct, ++t) {
+      for (int ct = seg_c0(sg); ct < s1; ++ct, ++t) {
         double2* T = Tb + (size_t)(t % 3) * TE;
 #ifdef SLSHT_WS_TRACE
         const bool tr = LP.trace && blockIdx.x == 0 && c_tid == 0 && t < 128;
@@ -348,7 +359,7 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
 #endif
         __syncwarp();
         if (lane == 0) mbar_arrive(&wempty[sl]);
-        if (ct == nct - 1 && lane == 0) mbar_arrive(uempty);
+        if (ct == s1 - 1 && lane == 0) mbar_arrive(uempty);
         // first DIF stage (radix R1, span N) on the accumulators: rows cw + k MP, twiddle
         // rou^(cw k)
 #pragma unroll
@@ -376,8 +387,9 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
 #ifdef SLSHT_WS_TRACE
         if (tr) LP.trace[t * 8 + 5] = clock64();
 #endif
-        FftDifDigest<N, MP, NT, MT * NT, NC>::run(T, rou_s, c_tid, 1, ct * NT, P.ncol, ncomp,
-                                                  betaw_s, a0, D);  // ends with a sync
+        // the warm-up tile before the unit's range adds nothing to the digest
+        FftDifDigest<N, MP, NT, MT * NT, NC>::run(T, rou_s, c_tid, 1, ct * NT, P.ncol,
+                                                  ct < s0 ? 0 : ncomp, betaw_s, a0, D);
 #ifdef SLSHT_WS_TRACE
         if (tr) LP.trace[t * 8 + 6] = clock64();
 #endif
@@ -413,17 +425,10 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
             const double x = dpart[(ip * MT + c) * 8 + f];
             s = (f == 1) ? fmax(s, x) : s + x;
           }
-          const CompRec rec = P.comps[g * MT + c];
-          if (f == 1) s = sqrt(s);
-          if (f >= 6) s *= 1.0 / ((double)N * N * N);
-          LP.digest[(size_t)(rec.l * rec.l + rec.l + rec.m) * 8 + f] = s;
-          if (P.mirror && rec.m > 0) {
-            const double sg = (rec.m & 1) ? -1.0 : 1.0;
-            const double sm = f < 2 ? s : ((f & 1) ? -(sg * s) : sg * s);  // (-1)^m conj
-            LP.digest[(size_t)(rec.l * rec.l + rec.l - rec.m) * 8 + f] = sm;
-          }
+          // the unit's partial (max |g|^2, unscaled integrals): k_digest finishes the row
+          LP.partials[((size_t)(g * MT + c) * LP.nseg + sg) * 8 + f] = s;
         }
-        named_sync(1, NC);  // dpart reused by the next group
+        named_sync(1, NC);  // dpart reused by the next unit
       }
     }
     return;
@@ -441,7 +446,9 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
   const int ncol = P.ncol;
   const long long sbit = (long long)0x8000000000000000ULL;
   long long t = 0;
-  for (int g = blockIdx.x; g < LP.n_groups; g += gridDim.x) {
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const int g = u / LP.nseg, sg = u % LP.nseg;
+    const int s0 = seg_lo(sg), s1 = seg_lo(sg + 1);
     const int ncomp = min(MT, P.count - g * MT);
     bool act = c < ncomp;
     long long base = 0;
@@ -457,19 +464,20 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
     }
     const int ksh0 = (int)(base & 7);
     double2* outp = P.out + base;
-    for (int ct = 0; ct < nct; ++ct, ++t) {
+    for (int ct = seg_c0(sg); ct < s1; ++ct, ++t) {
       const int C = ct * NT;
       mbar_wait(&tready[t & 1], (uint32_t)((t >> 1) & 1));
 #ifdef SLSHT_WS_TRACE
       const bool tr = LP.trace && blockIdx.x == 0 && st == 0 && t < 128;
 #endif
 #ifndef LN_NO_STORE
-      if (act) {
+      if (act && ct >= s0) {
         const double2* Tc = Tb + (size_t)(t % 3) * TE + (size_t)c * N * NT;
         const double2* Tp = Tb + (size_t)((t + 2) % 3) * TE + (size_t)c * N * NT + 8;
         double2* orow = outp + C;  // row a: orow + a ncol
         if (ct > 0 && ct < nct - 1) {
-          // interior tile: every element of every line exists
+          // interior tile: every element of every line exists (the previous tile is resident,
+          // also at a unit's first tile: the unit computed it)
 #pragma unroll
           for (int a = 0; a < N; ++a) {
             const int d = j - ((ksh0 + a) & 7);  // column offset from C (< 0: previous tile)
@@ -480,17 +488,18 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
             orow[a * ncol + d] = v;
           }
         } else {
+          // the row's first tile (the line's head is in row a - 1: written with that row's last
+          // tile) and last tile (one column); stores predicated, loads always in range
           const int cmax = ncol - C;  // columns of this tile in the row
 #pragma unroll
           for (int a = 0; a < N; ++a) {
             const int d = j - ((ksh0 + a) & 7);
-            if (d >= 0 ? d < cmax : ct > 0) {
-              const double2* src = (d < 0 ? Tp : Tc) + kPerm.v[a] * NT + d;
-              double2 v = *src;
-              v = make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ fr),
-                               __longlong_as_double(__double_as_longlong(v.y) ^ fi));
-              orow[a * ncol + d] = v;
-            }
+            const bool ok = d >= 0 ? d < cmax : ct > 0;
+            const double2* src = (d < 0 ? Tp : Tc) + kPerm.v[a] * NT + d;
+            double2 v = *src;
+            v = make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ fr),
+                             __longlong_as_double(__double_as_longlong(v.y) ^ fi));
+            if (ok) orow[a * ncol + d] = v;
           }
         }
       }

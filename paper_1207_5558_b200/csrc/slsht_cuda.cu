@@ -105,6 +105,8 @@ struct slsht_cuda_plan {
   void (*lines_fn)(LnParams) = nullptr;
   int lines_threads = 0;
   int lines_upad = 0;
+  int lines_nseg = 1;  // column segments per component group (fixed per n: digests do not
+                       // depend on chunking or sharding)
   int lines_urb[136] = {};
   int* d_ubase = nullptr;  // stage-tiled U layout (ws path): per (p, q) row block offset
   int* d_ustr = nullptr;   //   and row stride
@@ -327,17 +329,15 @@ void build_plan(slsht_cuda_plan* p) {
     p->n_slots = 2LL * per * ch;
   }
   couple_tile(p->n, p->MG, p->NG);
-  // line-aligned kernel: whole component groups per CTA, so it needs enough groups per chunk
-  // to balance over the SMs (B200: 148); SLSHT_CUDA_LINES=0/1 forces it off/on
-  bool lines = false;
-  if ((p->ncol % 8) == 1 && p->n == 33) {
-    const long long groups = (p->max_chunk + 7) / 8, sms = 148;
-    const double eff = (double)groups / (double)(((groups + sms - 1) / sms) * sms);
-    lines = eff >= 0.85;
-    if (const char* e = std::getenv("SLSHT_CUDA_LINES")) lines = e[0] == '1';
-  }
+  // line-aligned kernel for n = 33 (ncol == 1 mod 8); SLSHT_CUDA_LINES=0 selects the
+  // column-strip kernel instead. Work units are (component group, one of 4 column segments):
+  // fine enough to balance a ring chunk or a degree shard over the SMs, and a fixed split, so
+  // the digests are bitwise independent of chunking and sharding.
+  bool lines = (p->ncol % 8) == 1 && p->n == 33;
+  if (const char* e = std::getenv("SLSHT_CUDA_LINES")) lines = lines && e[0] != '0';
   if (lines) {
     p->use_lines = true;
+    p->lines_nseg = std::min(4, (p->ncol + 7) / 8);
     p->MG = 1;
     p->NG = 1;
     p->lines_fn = k_couple_lines<33>;
@@ -700,9 +700,10 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     lp.group_elems = p->ws_stages.group_elems;
     for (int i = 0; i < p->n; ++i) lp.urb[i] = p->lines_urb[i];
     lp.n_groups = (ch.count + 7) / 8;
-    lp.digest = p->d_digest;
+    lp.nseg = p->lines_nseg;
+    lp.partials = p->d_partials;
     lp.trace = nullptr;
-    const int grid = std::min(lp.n_groups, p->num_sms);
+    const int grid = std::min(lp.n_groups * lp.nseg, p->num_sms);
 #ifdef SLSHT_WS_TRACE
     static long long* d_ltrace = nullptr;
     if (!d_ltrace) CK(cudaMalloc(&d_ltrace, 1024 * sizeof(long long)));
@@ -716,7 +717,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
       CK(cudaMemcpyAsync(h, d_ltrace, sizeof(h), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       fprintf(stderr, "lines grid %d groups %d\n", grid, lp.n_groups);
-      for (int k = 0; k < 80; ++k) {
+      for (int k = 0; k < 60; ++k) {
         const long long* r = h + 8 * k;
         fprintf(stderr, "tile %3d: start %8lld tfree %5lld wfull %5lld mma %5lld radix %5lld sync %5lld last %5lld | stores_done %8lld\n",
                 k, r[0] - h[0], r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4], r[6] - r[5], r[7] - h[0]);
@@ -764,13 +765,12 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   }
   CKL();
   record(p, 3);
-  if (!p->use_lines) {  // the line kernel writes the digests itself
-    k_digest<<<(ch.count + 3) / 4, 128, 0, s>>>(comps, ch.count, p->n_col_tiles, p->n,
-                                                    p->d_partials, p->mirror, p->d_digest);
-    CKL();
-  }
+  k_digest<<<(ch.count + 3) / 4, 128, 0, s>>>(comps, ch.count,
+                                                  p->use_lines ? p->lines_nseg : p->n_col_tiles,
+                                                  p->n, p->d_partials, p->mirror, p->d_digest);
+  CKL();
   record(p, 4);
-  p->launches += p->use_lines ? 3 : 4;
+  p->launches += 4;
   if (p->profile) {
     accumulate(p, ST_LEGENDRE, 0, 1);
     accumulate(p, ST_MODGEMM, 1, 2);
