@@ -595,6 +595,8 @@ void build_plan(slsht_cuda_plan* p) {
     CK(cudaFuncSetAttribute(couple_kernel(p->n, p->MG, p->NG),
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->couple_smem));
   }
+  if (const char* e = std::getenv("SLSHT_CUDA_NSEG"))  // experiments: segments per group
+    p->lines_nseg = std::max(1, std::min(std::atoi(e), (p->ncol + 7) / 8));
   if (p->couple_smem > (size_t)prop.sharedMemPerBlockOptin)
     throw Status{SLSHT_ERR_VALIDATION, "window band limit too large for the shared-memory tile"};
   CK(cudaStreamSynchronize(s));
