@@ -230,15 +230,17 @@ __global__ void __launch_bounds__(1024) k_delta(int L, double* __restrict__ delt
   }
 }
 
+// Shared memory of k_delta for band limit L (the opt-in attribute is set by configure_delta,
+// outside any stream capture).
+inline size_t delta_smem(int L) { return sizeof(double) * (size_t)(L + 1) * (L + 2); }
+inline cudaError_t configure_delta(int L) {
+  if (delta_smem(L) > 227 * 1024) return cudaErrorInvalidValue;
+  return cudaFuncSetAttribute(k_delta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)delta_smem(L));
+}
 // Launch k_delta for band limit L on stream s (one CTA).
 inline cudaError_t launch_delta(int L, double* out, cudaStream_t s) {
-  const size_t T = (size_t)(L + 1) * (L + 2) / 2;
-  const size_t bytes = sizeof(double) * 2 * T;
-  if (bytes > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(k_delta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)bytes);
-  if (e != cudaSuccess) return e;
-  k_delta<<<1, 1024, bytes, s>>>(L, out);
+  k_delta<<<1, 1024, delta_smem(L), s>>>(L, out);
   return cudaGetLastError();
 }
 

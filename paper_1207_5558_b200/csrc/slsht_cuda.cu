@@ -115,6 +115,8 @@ struct slsht_cuda_plan {
   cudaStream_t aux_stream = nullptr;  // window-table chain of the setup, overlapped
   cudaEvent_t ev_fork = nullptr, ev_wtab = nullptr;
   bool wtab_pending = false;
+  cudaGraphExec_t graph = nullptr;  // forward_device replay (setup + every chunk), built once
+  long long graph_launches = 0;
   bool own_stream = false;
   bool profile = false;
   std::string last_error;
@@ -199,6 +201,7 @@ void free_plan(slsht_cuda_plan* p) {
     cudaStreamSynchronize(p->aux_stream);
     cudaStreamDestroy(p->aux_stream);
   }
+  if (p->graph) cudaGraphExecDestroy(p->graph);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_wtab) cudaEventDestroy(p->ev_wtab);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
@@ -578,6 +581,8 @@ void build_plan(slsht_cuda_plan* p) {
 
   p->num_sms = prop.multiProcessorCount;
   CK(cudaFuncSetAttribute(k_modgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM));
+  if (configure_delta(L) != cudaSuccess)
+    throw Status{SLSHT_ERR_VALIDATION, "window band limit too large for the on-chip Delta recursion"};
   for (int c0 = 0; c0 < p->NPQ; c0 += MG_COLS) {  // distinct q per modulated-SHT column tile
     const int c1 = std::min(p->NPQ, c0 + MG_COLS) - 1;
     if (pq[2 * c1] - pq[2 * c0] + 1 > MG_NQ)
@@ -877,9 +882,37 @@ int slsht_cuda_forward_device(slsht_cuda_plan* p, const double* f, const double*
     p->launches = 0;
     for (double& v : p->stage_ms) v = 0.0;
     load_inputs(p, f, h, inputs_on_device != 0);
-    run_setup(p);
-    for (const Chunk& ch : p->chunks) run_chunk(p, ch);
-    join_aux(p);
+    // The device work only touches plan-owned buffers, so it is captured once into a CUDA graph
+    // (both streams, with their fork/join events) and replayed: no per-kernel launch overhead.
+    // Stage profiling needs the events between kernels, so it runs the stream path.
+    const bool use_graph = !p->profile && std::getenv("SLSHT_CUDA_NO_GRAPH") == nullptr;
+    if (use_graph && !p->graph) {
+      CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+      cudaGraph_t graph = nullptr;
+      try {
+        run_setup(p);
+        for (const Chunk& ch : p->chunks) run_chunk(p, ch);
+        join_aux(p);
+      } catch (...) {
+        cudaStreamEndCapture(p->stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      CK(cudaStreamEndCapture(p->stream, &graph));
+      const cudaError_t e = cudaGraphInstantiate(&p->graph, graph, 0);
+      cudaGraphDestroy(graph);
+      CK(e);
+      p->graph_launches = p->launches;
+      p->launches = 0;
+    }
+    if (use_graph) {
+      CK(cudaGraphLaunch(p->graph, p->stream));
+      p->launches += p->graph_launches;
+    } else {
+      run_setup(p);
+      for (const Chunk& ch : p->chunks) run_chunk(p, ch);
+      join_aux(p);
+    }
     if (digests) copy_digests(p, digests, digests_on_device != 0);
     if (synchronize) check_numeric(p);
   });
@@ -1030,6 +1063,7 @@ int slsht_cuda_delta_tables(int device, int L, double* out) {
     double* d = dalloc<double>(dsz);
     if ((size_t)(L + 1) * (L + 2) * 8 > 227 * 1024)
       throw Status{SLSHT_ERR_VALIDATION, "band limit too large for the on-chip Delta recursion"};
+    CK(configure_delta(L));
     CK(launch_delta(L, d, 0));
     CK(cudaMemcpy(out, d, dsz * sizeof(double), cudaMemcpyDeviceToHost));
     CK(cudaFree(d));
