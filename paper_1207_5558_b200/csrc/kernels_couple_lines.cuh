@@ -100,6 +100,10 @@ struct LnCfg {
     return r;
   }();
   static constexpr int LAST_ITEMS = MT * NT * (N / RLAST);  // butterflies of the last stage
+  // the last stage runs on the first NFW compute warps only (one butterfly per thread); the
+  // other compute warps go on to the next tile's DMMA meanwhile
+  static constexpr int NFW = LAST_ITEMS / 32;
+  static constexpr int NF = NFW * 32;
   static constexpr int NPART = LAST_ITEMS / (MT * NT);       // digest partials per component
   static constexpr size_t TAB_BYTES = (size_t)N * 16 + (size_t)(L + 1) * 8 + (size_t)(N + 2) * 4 +
                                       (size_t)N * 4 + 16 + MT * 24 + (size_t)NPART * MT * 8 * 8;
@@ -107,7 +111,7 @@ struct LnCfg {
   static constexpr int NBAR = 2 + 4 + 4;  // ufull uempty | wfull[2] wempty[2] | tready[2] tfree[2]
   static constexpr size_t SMEM = OFF_BAR + NBAR * 8;
   static_assert(R1 < N, "the fused first stage needs a composite length");
-  static_assert(LAST_ITEMS <= NC, "one last-stage butterfly per compute thread");
+  static_assert(LAST_ITEMS <= NC && LAST_ITEMS % 32 == 0, "one butterfly per FFT thread");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -199,6 +203,28 @@ struct FftDifDigest {
   }
 };
 
+// Warp -> first-stage row group: the FFT warps (the first NFW) take the groups with the fewest
+// k-steps, since they also run the last stage.
+template <int N>
+struct LnGroupMap {
+  int v[LnCfg<N>::MP];
+  constexpr LnGroupMap() : v() {
+    using Rows = LnRows<N>;
+    constexpr int MP = LnCfg<N>::MP, R1 = LnCfg<N>::R1;
+    int ks[MP] = {};
+    for (int r = 0; r < MP; ++r)
+      for (int k = 0; k < R1; ++k) ks[r] += (Rows::np(Rows::jq_of_row(r + k * MP)) + 3) / 4;
+    bool used[MP] = {};
+    for (int i = 0; i < MP; ++i) {  // stable selection by ascending k-step count
+      int best = -1;
+      for (int r = 0; r < MP; ++r)
+        if (!used[r] && (best < 0 || ks[r] < ks[best])) best = r;
+      used[best] = true;
+      v[i] = best;
+    }
+  }
+};
+
 // DMMA chains of first-stage row group CW (T rows CW + k MP, k < R1): Gauss 3-product complex
 // MMA over the k-steps of each row's q block. Every row offset and k-step count is a
 // compile-time constant (the warp dispatches on its group once per tile), so the loop has no
@@ -282,7 +308,7 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
     for (int b = 0; b < 2; ++b) {
       mbar_init(&wfull[b], 1);
       mbar_init(&wempty[b], NCW);
-      mbar_init(&tready[b], NCW);
+      mbar_init(&tready[b], Cfg::NFW);
       mbar_init(&tfree[b], Cfg::NSW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -322,7 +348,10 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
 
   if (warp <= NCW) {
     // ------------------------------------------------------------------ compute warps
-    const int cw = warp - 1;  // row group: T rows cw + k MP, k < R1 (one first-stage butterfly)
+    constexpr LnGroupMap<N> kMap{};
+    constexpr int NF = Cfg::NF;
+    const int cw = kMap.v[warp - 1];  // row group: T rows cw + k MP, k < R1
+    const bool fft = warp - 1 < Cfg::NFW;
     const int c_tid = tid - 32;
     const int kl = lane & 3, ar = lane >> 2;
     const int a0 = dif_last_freq0<N, Cfg::RLAST>(c_tid / (MT * NT));
@@ -387,14 +416,16 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
 #ifdef SLSHT_WS_TRACE
         if (tr) LP.trace[t * 8 + 5] = clock64();
 #endif
+        if (!fft) continue;  // on to the next tile's DMMA
         // the warm-up tile before the unit's range adds nothing to the digest
-        FftDifDigest<N, MP, NT, MT * NT, NC>::run(T, rou_s, c_tid, 1, ct * NT, P.ncol,
+        FftDifDigest<N, MP, NT, MT * NT, NF>::run(T, rou_s, c_tid, 2, ct * NT, P.ncol,
                                                   ct < s0 ? 0 : ncomp, betaw_s, a0, D);
 #ifdef SLSHT_WS_TRACE
         if (tr) LP.trace[t * 8 + 6] = clock64();
 #endif
         if (lane == 0) mbar_arrive(&tready[t & 1]);
       }
+      if (!fft) continue;
       // ---------------- digest rows of the group: 8-lane shuffle tree, then NPART partials
       {
         constexpr int LI = Cfg::LAST_ITEMS;  // thread c_tid < LI holds pair c_tid % 64
@@ -416,7 +447,7 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
 #pragma unroll
           for (int f = 0; f < 8; ++f) dpart[(ip * MT + c) * 8 + f] = v[f];
         }
-        named_sync(1, NC);
+        named_sync(2, NF);
         if (c_tid < ncomp * 8) {
           const int c = c_tid >> 3, f = c_tid & 7;
           double s = 0.0;
@@ -428,7 +459,7 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
           // the unit's partial (max |g|^2, unscaled integrals): k_digest finishes the row
           LP.partials[((size_t)(g * MT + c) * LP.nseg + sg) * 8 + f] = s;
         }
-        named_sync(1, NC);  // dpart reused by the next unit
+        named_sync(2, NF);  // dpart reused by the next unit
       }
     }
     return;
