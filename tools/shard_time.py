@@ -28,7 +28,7 @@ for world in (1, 2, 4, 8):
         l0, l1 = C.shard_degrees(cfg, world, r)
         mat = cfg.samples() * 16 / world < 40e9
         with S.Plan(cfg.L_f, cfg.L_h, real_mode=cfg.real_mode, l_begin=l0, l_end=l1,
-                    materialize=mat, ring_bytes=2048 << 20) as p:
+                    materialize=mat, ring_bytes=16384 << 20) as p:
             for _ in range(2):
                 p.forward_device(fd.data_ptr(), hd.data_ptr(), inputs_on_device=True,
                                  digests_ptr=dig.data_ptr(), digests_on_device=True)

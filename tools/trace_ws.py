@@ -6,5 +6,5 @@ import os; L.LIB_PATH = Path(os.environ.get('TRACE_LIB', '/root/repo/tools/libsl
 import paper_1207_5558_b200 as S
 from paper_1207_5558_b200 import configs as C
 f, h, cfg = C.make_inputs(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
-with S.Plan(cfg.L_f, cfg.L_h, real_mode=cfg.real_mode, materialize=cfg.samples() * 16 < 40e9, ring_bytes=2048 << 20) as p:
+with S.Plan(cfg.L_f, cfg.L_h, real_mode=cfg.real_mode, materialize=cfg.samples() * 16 < 40e9, ring_bytes=16384 << 20) as p:
     p.forward_digests(f, h)
