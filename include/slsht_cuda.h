@@ -116,6 +116,12 @@ int slsht_cuda_stage_times(const slsht_cuda_plan* plan, double* out_ms, int n);
  * synchronization per chunk while on). */
 int slsht_cuda_set_profiling(slsht_cuda_plan* plan, int enable);
 
+/* Device time (ms) of the coupling kernel in the last forward_device of a single-chunk
+ * (materialized) plan, from CUDA events recorded around it on the plan's stream on every call
+ * (also inside its CUDA graph). Blocks until that kernel has finished. SLSHT_ERR_VALIDATION if
+ * the plan has several chunks or has not run forward_device. */
+int slsht_cuda_kernel_time(const slsht_cuda_plan* plan, double* ms);
+
 /* Component-level entry points (host arrays in/out), mirroring the reference's
  * DeltaTables (wigner.cpp:28-80), ModulatedSht::compute (transform.cpp:189-220) and the
  * window-side table of the coupling stage; used by the parity tests. */

@@ -35,6 +35,7 @@ EXPORTS = [
     "slsht_cuda_launch_count",
     "slsht_cuda_stage_times",
     "slsht_cuda_set_profiling",
+    "slsht_cuda_kernel_time",
     "slsht_cuda_delta_tables",
     "slsht_cuda_modulated",
 ]
@@ -100,6 +101,8 @@ def load() -> C.CDLL:
     lib.slsht_cuda_stage_times.restype = C.c_int
     lib.slsht_cuda_set_profiling.argtypes = [C.c_void_p, C.c_int]
     lib.slsht_cuda_set_profiling.restype = C.c_int
+    lib.slsht_cuda_kernel_time.argtypes = [C.c_void_p, _dp]
+    lib.slsht_cuda_kernel_time.restype = C.c_int
     lib.slsht_cuda_delta_tables.argtypes = [C.c_int, C.c_int, _dp]
     lib.slsht_cuda_delta_tables.restype = C.c_int
     lib.slsht_cuda_modulated.argtypes = [C.c_void_p, C.c_void_p, C.c_int, _ip, _ip, _dp]

@@ -156,6 +156,10 @@ struct slsht_cuda_plan {
   size_t stage_bytes = 0;
   cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
   cudaEvent_t ev_stage[ST_COUNT + 1] = {};
+  // single-chunk plans: the coupling kernel's start and end, recorded on every call (also
+  // inside the CUDA graph), read lazily by slsht_cuda_kernel_time
+  cudaEvent_t ev_lazy[2] = {};
+  bool lazy_valid = false;
 };
 
 namespace {
@@ -195,6 +199,8 @@ void free_plan(slsht_cuda_plan* p) {
     if (p->ev_copied[i]) cudaEventDestroy(p->ev_copied[i]);
   }
   for (auto& e : p->ev_stage)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : p->ev_lazy)
     if (e) cudaEventDestroy(e);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->aux_stream) {
@@ -578,6 +584,7 @@ void build_plan(slsht_cuda_plan* p) {
     CK(cudaEventCreateWithFlags(&p->ev_copied[i], cudaEventDisableTiming));
   }
   for (auto& e : p->ev_stage) CK(cudaEventCreate(&e));
+  for (auto& e : p->ev_lazy) CK(cudaEventCreate(&e));
 
   p->num_sms = prop.multiProcessorCount;
   CK(cudaFuncSetAttribute(k_modgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM));
@@ -609,6 +616,19 @@ void build_plan(slsht_cuda_plan* p) {
 
 void record(slsht_cuda_plan* p, int idx) {
   if (p->profile) CK(cudaEventRecord(p->ev_stage[idx], p->stream));
+}
+
+// Coupling-kernel boundary of a single-chunk plan (0: start, 1: end).
+void record_lazy(slsht_cuda_plan* p, int lazy_idx) {
+  if (p->chunks.size() != 1) return;
+  // inside a stream capture an external record becomes an event-record node, so graph replays
+  // record it too (a plain record would only order the capture)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(p->stream, &cs));
+  if (cs == cudaStreamCaptureStatusActive)
+    CK(cudaEventRecordWithFlags(p->ev_lazy[lazy_idx], p->stream, cudaEventRecordExternal));
+  else
+    CK(cudaEventRecord(p->ev_lazy[lazy_idx], p->stream));
 }
 
 void accumulate(slsht_cuda_plan* p, int st, int a, int b) {
@@ -678,6 +698,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   CKL();
   join_aux(p);
   record(p, 2);
+  record_lazy(p, 0);
   CoupleParams prm{};
   prm.U = p->d_U;
   prm.W = p->d_W;
@@ -772,6 +793,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   }
   CKL();
   record(p, 3);
+  record_lazy(p, 1);
   k_digest<<<(ch.count + 3) / 4, 128, 0, s>>>(comps, ch.count,
                                                   p->use_lines ? p->lines_nseg : p->n_col_tiles,
                                                   p->n, p->d_partials, p->mirror, p->d_digest);
@@ -884,7 +906,8 @@ int slsht_cuda_forward_device(slsht_cuda_plan* p, const double* f, const double*
     load_inputs(p, f, h, inputs_on_device != 0);
     // The device work only touches plan-owned buffers, so it is captured once into a CUDA graph
     // (both streams, with their fork/join events) and replayed: no per-kernel launch overhead.
-    // Stage profiling needs the events between kernels, so it runs the stream path.
+    // A single-chunk graph carries its stage events as event-record nodes, so every call's
+    // stage times are available (slsht_cuda_stage_times); profiling takes the stream path.
     const bool use_graph = !p->profile && std::getenv("SLSHT_CUDA_NO_GRAPH") == nullptr;
     if (use_graph && !p->graph) {
       CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
@@ -905,6 +928,7 @@ int slsht_cuda_forward_device(slsht_cuda_plan* p, const double* f, const double*
       p->graph_launches = p->launches;
       p->launches = 0;
     }
+    p->lazy_valid = p->chunks.size() == 1;
     if (use_graph) {
       CK(cudaGraphLaunch(p->graph, p->stream));
       p->launches += p->graph_launches;
@@ -1047,6 +1071,18 @@ int slsht_cuda_stage_times(const slsht_cuda_plan* p, double* out_ms, int n) {
   const int k = std::min(n, (int)ST_COUNT);
   for (int i = 0; i < k; ++i) out_ms[i] = p->stage_ms[i];
   return k;
+}
+
+int slsht_cuda_kernel_time(const slsht_cuda_plan* p, double* ms_out) {
+  if (!p || !ms_out || !p->lazy_valid) return SLSHT_ERR_VALIDATION;
+  float ms = 0.f;
+  if (cudaEventSynchronize(p->ev_lazy[1]) != cudaSuccess ||
+      cudaEventElapsedTime(&ms, p->ev_lazy[0], p->ev_lazy[1]) != cudaSuccess) {
+    cudaGetLastError();  // leave no error behind for the caller's runtime
+    return SLSHT_ERR_DEVICE;
+  }
+  *ms_out = ms;
+  return SLSHT_OK;
 }
 
 int slsht_cuda_delta_tables(int device, int L, double* out) {

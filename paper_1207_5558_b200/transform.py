@@ -166,6 +166,12 @@ class Plan:
     def set_profiling(self, enable: bool) -> None:
         self.lib.slsht_cuda_set_profiling(self.handle, int(enable))
 
+    def kernel_time(self) -> float | None:
+        """Coupling-kernel device time (ms) of the last forward_device (single-chunk plans)."""
+        out = C.c_double(0.0)
+        rc = self.lib.slsht_cuda_kernel_time(self.handle, C.byref(out))
+        return float(out.value) if rc == 0 else None
+
     def stage_times(self) -> list[float]:
         out = (C.c_double * 8)()
         k = self.lib.slsht_cuda_stage_times(self.handle, out, 8)
