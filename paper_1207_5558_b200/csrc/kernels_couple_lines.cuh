@@ -38,7 +38,8 @@ struct LnParams {
   int urb[136];           // per q row jq: offset of its padded row block in a U row
   int n_groups;
   int nseg;               // column segments per group: a work unit is (group, segment)
-  double* partials;       // [component][segment][8] digest partials (k_digest reduces them)
+  int nseg_dig;           // digest segments per group (a fixed split; nseg divides it)
+  double* partials;       // [component][digest segment][8] partials (k_digest reduces them)
   long long* trace;       // debug (SLSHT_WS_TRACE builds)
 };
 
@@ -321,6 +322,9 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
   const int n_units = LP.n_groups * LP.nseg;
   auto seg_lo = [&](int sg) { return (int)(((long long)sg * nct) / LP.nseg); };
   auto seg_c0 = [&](int sg) { return sg > 0 ? seg_lo(sg) - 1 : 0; };
+  // digest segments: a fixed split of every group's tiles, refined by the execution split, so
+  // the digest partials (and their sums) do not depend on how the work is cut into units
+  auto dig_lo = [&](int k) { return (int)(((long long)k * nct) / LP.nseg_dig); };
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
@@ -362,6 +366,8 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
       const int s0 = seg_lo(sg), s1 = seg_lo(sg + 1);
       const int ncomp = min(MT, P.count - g * MT);
       DigestAcc D{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0};
+      int kd = sg * (LP.nseg_dig / LP.nseg);  // digest segment of tile s0
+      int kd_end = dig_lo(kd + 1);
       mbar_wait(ufull, uphase);
       uphase ^= 1;
       for (int ct = seg_c0(sg); ct < s1; ++ct, ++t) {
@@ -424,42 +430,41 @@ __global__ void __launch_bounds__(LnCfg<N>::NTHREADS, 1) k_couple_lines(const Ln
         if (tr) LP.trace[t * 8 + 6] = clock64();
 #endif
         if (lane == 0) mbar_arrive(&tready[t & 1]);
-      }
-      if (!fft) continue;
-      // ---------------- digest rows of the group: 8-lane shuffle tree, then NPART partials
-      {
-        constexpr int LI = Cfg::LAST_ITEMS;  // thread c_tid < LI holds pair c_tid % 64
-        const unsigned m8 = 0xffu << (lane & ~7);
-        double v[8] = {D.s2, __longlong_as_double(D.mx2), D.pr, D.pi, D.g0r, D.g0i, D.ir, D.ii};
-        if (c_tid >= LI) {
+        if (ct < s0) continue;
+        // end of a digest segment: its partial (8-lane shuffle trees, then the NPART partial
+        // blocks in order; max |g|^2 and unscaled integrals, k_digest finishes the row)
+        if (ct + 1 == kd_end) {
+          constexpr int LI = Cfg::LAST_ITEMS;  // thread c_tid < LI holds pair c_tid % 64
+          const unsigned m8 = 0xffu << (lane & ~7);
+          double v[8] = {D.s2, __longlong_as_double(D.mx2), D.pr, D.pi, D.g0r, D.g0i, D.ir, D.ii};
 #pragma unroll
-          for (int f = 0; f < 8; ++f) v[f] = 0.0;
-        }
+          for (int off = 4; off > 0; off >>= 1)
 #pragma unroll
-        for (int off = 4; off > 0; off >>= 1)
+            for (int f = 0; f < 8; ++f) {
+              const double o = __shfl_down_sync(m8, v[f], off, 8);
+              v[f] = (f == 1) ? fmax(v[f], o) : v[f] + o;
+            }
+          if ((lane & 7) == 0 && c_tid < LI) {
+            const int c = (c_tid % (MT * NT)) / NT, ip = c_tid / (MT * NT);
 #pragma unroll
-          for (int f = 0; f < 8; ++f) {
-            const double o = __shfl_down_sync(m8, v[f], off, 8);
-            v[f] = (f == 1) ? fmax(v[f], o) : v[f] + o;
+            for (int f = 0; f < 8; ++f) dpart[(ip * MT + c) * 8 + f] = v[f];
           }
-        if ((lane & 7) == 0 && c_tid < LI) {
-          const int c = (c_tid % (MT * NT)) / NT, ip = c_tid / (MT * NT);
+          named_sync(2, NF);
+          if (c_tid < ncomp * 8) {
+            const int c = c_tid >> 3, f = c_tid & 7;
+            double sacc = 0.0;
 #pragma unroll
-          for (int f = 0; f < 8; ++f) dpart[(ip * MT + c) * 8 + f] = v[f];
-        }
-        named_sync(2, NF);
-        if (c_tid < ncomp * 8) {
-          const int c = c_tid >> 3, f = c_tid & 7;
-          double s = 0.0;
-#pragma unroll
-          for (int ip = 0; ip < Cfg::NPART; ++ip) {
-            const double x = dpart[(ip * MT + c) * 8 + f];
-            s = (f == 1) ? fmax(s, x) : s + x;
+            for (int ip = 0; ip < Cfg::NPART; ++ip) {
+              const double x = dpart[(ip * MT + c) * 8 + f];
+              sacc = (f == 1) ? fmax(sacc, x) : sacc + x;
+            }
+            LP.partials[((size_t)(g * MT + c) * LP.nseg_dig + kd) * 8 + f] = sacc;
           }
-          // the unit's partial (max |g|^2, unscaled integrals): k_digest finishes the row
-          LP.partials[((size_t)(g * MT + c) * LP.nseg + sg) * 8 + f] = s;
+          named_sync(2, NF);  // dpart reused by the next flush
+          D = DigestAcc{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0};
+          ++kd;
+          kd_end = dig_lo(kd + 1);
         }
-        named_sync(2, NF);  // dpart reused by the next unit
       }
     }
     return;

@@ -105,8 +105,9 @@ struct slsht_cuda_plan {
   void (*lines_fn)(LnParams) = nullptr;
   int lines_threads = 0;
   int lines_upad = 0;
-  int lines_nseg = 1;  // column segments per component group (fixed per n: digests do not
-                       // depend on chunking or sharding)
+  int lines_nseg = 1;      // line kernel: column segments per group (execution split, per chunk)
+  int lines_nseg_dig = 1;  // digest segments per group (fixed per n: the digests do not depend
+                           // on the execution split, the chunking or the sharding)
   int lines_urb[136] = {};
   int* d_ubase = nullptr;  // stage-tiled U layout (ws path): per (p, q) row block offset
   int* d_ustr = nullptr;   //   and row stride
@@ -346,7 +347,8 @@ void build_plan(slsht_cuda_plan* p) {
   if (const char* e = std::getenv("SLSHT_CUDA_LINES")) lines = lines && e[0] != '0';
   if (lines) {
     p->use_lines = true;
-    p->lines_nseg = std::min(4, (p->ncol + 7) / 8);
+    p->lines_nseg_dig = std::min(4, (p->ncol + 7) / 8);
+    p->lines_nseg = p->lines_nseg_dig;
     p->MG = 1;
     p->NG = 1;
     p->lines_fn = k_couple_lines<33>;
@@ -607,8 +609,26 @@ void build_plan(slsht_cuda_plan* p) {
     CK(cudaFuncSetAttribute(couple_kernel(p->n, p->MG, p->NG),
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->couple_smem));
   }
-  if (const char* e = std::getenv("SLSHT_CUDA_NSEG"))  // experiments: segments per group
-    p->lines_nseg = std::max(1, std::min(std::atoi(e), (p->ncol + 7) / 8));
+  if (p->use_lines) {
+    // execution split: the divisor of the digest split with the best balance over the SMs for
+    // a full chunk (each extra segment costs a warm-up tile per group)
+    const int nct = p->n_col_tiles, G = (p->max_chunk + 7) / 8, sms = p->num_sms;
+    double best = -1.0;
+    for (int ns = 1; ns <= p->lines_nseg_dig; ++ns) {
+      if (p->lines_nseg_dig % ns) continue;
+      const long long units = (long long)G * ns, rounds = (units + sms - 1) / sms;
+      const double eff = (double)units / (double)(rounds * sms) *
+                         (double)nct / (double)(nct + ns - 1);
+      if (eff > best + 1e-9) {
+        best = eff;
+        p->lines_nseg = ns;
+      }
+    }
+    if (const char* e = std::getenv("SLSHT_CUDA_NSEG")) {  // experiments
+      const int ns = std::atoi(e);
+      if (ns >= 1 && p->lines_nseg_dig % ns == 0) p->lines_nseg = ns;
+    }
+  }
   if (p->couple_smem > (size_t)prop.sharedMemPerBlockOptin)
     throw Status{SLSHT_ERR_VALIDATION, "window band limit too large for the shared-memory tile"};
   CK(cudaStreamSynchronize(s));
@@ -729,6 +749,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     for (int i = 0; i < p->n; ++i) lp.urb[i] = p->lines_urb[i];
     lp.n_groups = (ch.count + 7) / 8;
     lp.nseg = p->lines_nseg;
+    lp.nseg_dig = p->lines_nseg_dig;
     lp.partials = p->d_partials;
     lp.trace = nullptr;
     const int grid = std::min(lp.n_groups * lp.nseg, p->num_sms);
@@ -795,7 +816,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   record(p, 3);
   record_lazy(p, 1);
   k_digest<<<(ch.count + 3) / 4, 128, 0, s>>>(comps, ch.count,
-                                                  p->use_lines ? p->lines_nseg : p->n_col_tiles,
+                                                  p->use_lines ? p->lines_nseg_dig : p->n_col_tiles,
                                                   p->n, p->d_partials, p->mirror, p->d_digest);
   CKL();
   record(p, 4);
