@@ -34,10 +34,85 @@ __device__ __forceinline__ void quad_weight_sum(int K, double angle, int lane, d
   }
 }
 
-__global__ void k_nodes(int N, double* __restrict__ ncos, double* __restrict__ nsin,
-                        double* __restrict__ weights, int L_h, double* __restrict__ betaw,
-                        int* __restrict__ err_flag) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+// The main-stream setup in one launch. Three independent parts, each computing the node
+// angles it needs with the same expression (so the values are identical), run side by side:
+//   blocks [0, ni): the I-table I(theta_j, mu) = 2 pi conj(sum_l f_l^mu lambda_l^mu(theta_j))
+//     (transform.cpp:158-173), per (node block, order mu), recursion coefficients and f_l^mu
+//     staged in shared memory;
+//   blocks [ni, ni + nw): the window rows lambda_p^q(theta_j), q-major (p, q) rows
+//     c = qoff[q+L] + p-|q| (transform.cpp:175-186), per (node block, order q);
+//   the rest: theta nodes and weights, beta weights (4 warps = 4 weights per block).
+// Row strides are ld (>= n_nodes, the padding stays zero).
+struct SetupMainParams {
+  int N, L_h, L_f, n_nodes, ld, nbx, ni, nw;
+  const double* f;
+  const int* qoff;
+  double *ncos, *nsin, *weights, *betaw, *lamh, *itab;
+  int* err;
+};
+
+__device__ __forceinline__ void node_angle(int N, int j, double& c, double& s) {
+  const double theta = kPi * (2 * j + 1) / (2 * N + 1);
+  sincos(theta, &s, &c);
+}
+
+__global__ void __launch_bounds__(128) k_setup_main(const SetupMainParams P) {
+  extern __shared__ double coef[];
+  int b = blockIdx.x;
+  if (b < P.ni) {  // ---- I-table block (transform.cpp:158-173)
+    const int L_f = P.L_f;
+    double *sf = coef, *ca = coef + (L_f + 1), *cb = coef + 2 * (L_f + 1);
+    double2* fs = reinterpret_cast<double2*>(coef + 3 * (L_f + 1) + ((3 * (L_f + 1)) & 1));
+    const int mu = b / P.nbx - L_f;
+    const int amu = mu < 0 ? -mu : mu;
+    legendre_coeffs(amu, L_f, sf, ca, cb);
+    for (int l = amu + threadIdx.x; l <= L_f; l += blockDim.x)
+      fs[l] = *reinterpret_cast<const double2*>(P.f + 2 * (l * l + l + mu));
+    __syncthreads();
+    const int j = (b % P.nbx) * blockDim.x + threadIdx.x;
+    if (j >= P.n_nodes) return;
+    double c, s;
+    node_angle(P.N, j, c, s);
+    LegendreIt r;
+    r.seed(mu, c, s, sf);
+    double ar = 0.0, ai = 0.0;
+    for (int l = amu; l <= L_f; ++l) {
+      if (l > amu) r.next(ca, cb);
+      const double2 fv = fs[l];
+      ar += fv.x * r.cur;
+      ai += fv.y * r.cur;
+    }
+    double2 o;
+    o.x = 2.0 * kPi * ar;
+    o.y = -(2.0 * kPi * ai);
+    reinterpret_cast<double2*>(P.itab)[(size_t)(mu + L_f) * P.ld + j] = o;
+    return;
+  }
+  b -= P.ni;
+  if (b < P.nw) {  // ---- window Legendre rows lambda_p^q(theta_j) (transform.cpp:175-186)
+    const int L_h = P.L_h;
+    double *sf = coef, *ca = coef + (L_h + 1), *cb = coef + 2 * (L_h + 1);
+    const int q = b / P.nbx - L_h;
+    const int aq = q < 0 ? -q : q;
+    legendre_coeffs(aq, L_h, sf, ca, cb);
+    __syncthreads();
+    const int j = (b % P.nbx) * blockDim.x + threadIdx.x;
+    if (j >= P.n_nodes) return;
+    double c, s;
+    node_angle(P.N, j, c, s);
+    LegendreIt r;
+    r.seed(q, c, s, sf);
+    const int base = P.qoff[q + L_h];
+    for (int p = aq; p <= L_h; ++p) {
+      if (p > aq) r.next(ca, cb);
+      P.lamh[(size_t)(base + p - aq) * P.ld + j] = r.cur;
+    }
+    return;
+  }
+  b -= P.nw;
+  // ---- quadrature weights and node angles: one warp per weight (as k_nodes)
+  const int N = P.N, L_h = P.L_h;
+  const int w = (b * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w <= N) {
     const int t = w;
     const double theta = kPi * (2 * t + 1) / (2 * N + 1);
@@ -46,79 +121,25 @@ __global__ void k_nodes(int N, double* __restrict__ ncos, double* __restrict__ n
     if (lane == 0) {
       double s, c;
       sincos(theta, &s, &c);
-      ncos[t] = c;
-      nsin[t] = s;
-      if (fabs(si) >= 1e-12) atomicExch(err_flag, 1);
-      weights[t] = (t < N) ? 2.0 * sr / (2 * N + 1) : sr / (2 * N + 1);
+      P.ncos[t] = c;
+      P.nsin[t] = s;
+      if (fabs(si) >= 1e-12) atomicExch(P.err, 1);
+      P.weights[t] = (t < N) ? 2.0 * sr / (2 * N + 1) : sr / (2 * N + 1);
     }
   } else if (w - (N + 1) <= L_h) {
     const int t = w - (N + 1);
     const int L = L_h, n = 2 * L + 1;
     if (t == 0) {
-      if (lane == 0) betaw[0] = 4.0 * kPi * kPi / (L / 2 + 0.5);
+      if (lane == 0) P.betaw[0] = 4.0 * kPi * kPi / (L / 2 + 0.5);
     } else {
       double sr, si;
       quad_weight_sum(L, 2.0 * kPi * t / n, lane, sr, si);
       if (lane == 0) {
-        if (fabs(si) >= 1e-12) atomicExch(err_flag, 2);
-        betaw[t] = 8.0 * kPi * kPi * sr;
+        if (fabs(si) >= 1e-12) atomicExch(P.err, 2);
+        P.betaw[t] = 8.0 * kPi * kPi * sr;
       }
     }
   }
-}
-
-// lambda_p^q(theta_j) for the window band, rows in q-major (p, q) order: row c = qoff[q+L] + p-|q|,
-// row stride ld (>= n_nodes; the padding stays zero).
-// grid (node blocks, 2L_h+1 orders); dynamic smem 3 (L_h+1) doubles.
-__global__ void k_legendre_window(int L_h, int n_nodes, int ld, const double* __restrict__ ncos,
-                                  const double* __restrict__ nsin, const int* __restrict__ qoff,
-                                  double* __restrict__ lamh) {
-  extern __shared__ double coef[];
-  double *sf = coef, *ca = coef + (L_h + 1), *cb = coef + 2 * (L_h + 1);
-  const int q = (int)blockIdx.y - L_h;
-  const int aq = q < 0 ? -q : q;
-  legendre_coeffs(aq, L_h, sf, ca, cb);
-  __syncthreads();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_nodes) return;
-  LegendreIt r;
-  r.seed(q, ncos[j], nsin[j], sf);
-  const int base = qoff[q + L_h];
-  for (int p = aq; p <= L_h; ++p) {
-    if (p > aq) r.next(ca, cb);
-    lamh[(size_t)(base + p - aq) * ld + j] = r.cur;
-  }
-}
-
-// I(theta_j, mu) = 2 pi conj(sum_{l=|mu|}^{L_f} f_l^mu lambda_l^mu(theta_j)) (transform.cpp:158-173)
-// grid (node blocks, 2L_f+1 orders); dynamic smem 3 (L_f+1) doubles + (L_f+1) complex (f_l^mu).
-__global__ void k_itab(int L_f, int n_nodes, int ld, const double* __restrict__ ncos,
-                       const double* __restrict__ nsin, const double* __restrict__ f,
-                       double* __restrict__ itab) {
-  extern __shared__ double coef[];
-  double *sf = coef, *ca = coef + (L_f + 1), *cb = coef + 2 * (L_f + 1);
-  double2* fs = reinterpret_cast<double2*>(coef + 3 * (L_f + 1) + ((3 * (L_f + 1)) & 1));
-  const int mu = (int)blockIdx.y - L_f;
-  const int amu = mu < 0 ? -mu : mu;
-  legendre_coeffs(amu, L_f, sf, ca, cb);
-  for (int l = amu + threadIdx.x; l <= L_f; l += blockDim.x)
-    fs[l] = *reinterpret_cast<const double2*>(f + 2 * (l * l + l + mu));
-  __syncthreads();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_nodes) return;
-  LegendreIt r;
-  r.seed(mu, ncos[j], nsin[j], sf);
-  double ar = 0.0, ai = 0.0;
-  for (int l = amu; l <= L_f; ++l) {
-    if (l > amu) r.next(ca, cb);
-    const double2 fv = fs[l];
-    ar += fv.x * r.cur;
-    ai += fv.y * r.cur;
-  }
-  double2 o;
-  o.x = 2.0 * kPi * ar;
-  o.y = -(2.0 * kPi * ai);
-  reinterpret_cast<double2*>(itab)[(size_t)(mu + L_f) * ld + j] = o;
 }
 
 __device__ __forceinline__ size_t delta_offset(int p) {

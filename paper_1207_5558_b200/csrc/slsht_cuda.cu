@@ -676,16 +676,30 @@ void run_setup(slsht_cuda_plan* p) {
   record(p, 0);
   CK(cudaEventRecord(p->ev_fork, s));  // after the inputs' upload on s
   CK(cudaStreamWaitEvent(p->aux_stream, p->ev_fork, 0));
-  k_nodes<<<(p->n_nodes + L + 1 + 3) / 4, 128, 0, s>>>(p->N, p->d_ncos, p->d_nsin, p->d_weights,
-                                                       L, p->d_betaw, p->d_err);  // warp per weight
-  CKL();
-  k_legendre_window<<<dim3((p->n_nodes + 127) / 128, p->n), 128, 3 * (L + 1) * sizeof(double), s>>>(
-      L, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_qoff, p->d_lamh);
-  CKL();
-  k_itab<<<dim3((p->n_nodes + 127) / 128, 2 * p->L_f + 1), 128,
-           (5 * (p->L_f + 1) + 1) * sizeof(double), s>>>(
-      p->L_f, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_f, reinterpret_cast<double*>(p->d_itab));
-  CKL();
+  {
+    SetupMainParams sp{};
+    sp.N = p->N;
+    sp.L_h = L;
+    sp.L_f = p->L_f;
+    sp.n_nodes = p->n_nodes;
+    sp.ld = p->ldA;
+    sp.nbx = (p->n_nodes + 127) / 128;
+    sp.ni = sp.nbx * (2 * p->L_f + 1);
+    sp.nw = sp.nbx * p->n;
+    sp.f = p->d_f;
+    sp.qoff = p->d_qoff;
+    sp.ncos = p->d_ncos;
+    sp.nsin = p->d_nsin;
+    sp.weights = p->d_weights;
+    sp.betaw = p->d_betaw;
+    sp.lamh = p->d_lamh;
+    sp.itab = reinterpret_cast<double*>(p->d_itab);
+    sp.err = p->d_err;
+    const int nnodes_blocks = (p->n_nodes + L + 1 + 3) / 4;  // 4 warps (weights) per block
+    const size_t sm = sizeof(double) * std::max<size_t>(3 * (L + 1), 5 * (p->L_f + 1) + 1);
+    k_setup_main<<<sp.ni + sp.nw + nnodes_blocks, 128, sm, s>>>(sp);
+    CKL();
+  }
   cudaStream_t a = p->aux_stream;
   CK(launch_delta(L, p->d_delta, a));
   const int wmax = (2 * L + 1) * (2 * L + 1) * p->nb;
@@ -698,7 +712,7 @@ void run_setup(slsht_cuda_plan* p) {
   CKL();
   CK(cudaEventRecord(p->ev_wtab, a));
   p->wtab_pending = true;
-  p->launches += 6;
+  p->launches += 4;
   record(p, 1);
   accumulate(p, ST_SETUP, 0, 1);
 }
