@@ -340,9 +340,10 @@ void build_plan(slsht_cuda_plan* p) {
   }
   couple_tile(p->n, p->MG, p->NG);
   // line-aligned kernel for n = 33 (ncol == 1 mod 8); SLSHT_CUDA_LINES=0 selects the
-  // column-strip kernel instead. Work units are (component group, one of 4 column segments):
-  // fine enough to balance a ring chunk or a degree shard over the SMs, and a fixed split, so
-  // the digests are bitwise independent of chunking and sharding.
+  // column-strip kernel instead. Its digest partials use a fixed split of every component
+  // group's column tiles into 4 segments (so the digests are bitwise independent of the
+  // chunking and the sharding); its work units are (group, one of 1, 2 or 4 segments), chosen
+  // per plan for balance over the SMs.
   bool lines = (p->ncol % 8) == 1 && p->n == 33;
   if (const char* e = std::getenv("SLSHT_CUDA_LINES")) lines = lines && e[0] != '0';
   if (lines) {
