@@ -130,6 +130,18 @@ int slsht_cuda_delta_tables(int device, int L, double* out);
 int slsht_cuda_modulated(slsht_cuda_plan* plan, const double* f, int count, const int* l,
                          const int* m, double* out);
 
+/* Inversion from the SLSHT (transform.cpp:469-544: inverse_slsht / InverseAccumulator, the
+ * reference's tau3 stage): runs the forward on the device and returns
+ *   f_rec[coeff_index(l, m)] = integrate_volume(g(l, m)) / (sqrt(16 pi^3) h00),
+ * l <= signal_band_limit, from the digest epilogue's quadrature integrals (no volume leaves
+ * the device). Components not emitted (real mode without emit_negative_m) are filled by
+ * conjugate symmetry, as InverseAccumulator(fill_negative_by_symmetry = true) does.
+ * f_rec: coeff_count(signal_band_limit) complex (host memory).
+ * Errors: SLSHT_ERR_NUMERIC if |h00| <= 1e-10; SLSHT_ERR_VALIDATION if the plan does not
+ * cover every degree l <= signal_band_limit. */
+int slsht_cuda_inverse(slsht_cuda_plan* plan, const double* f, const double* h,
+                       double h00_re, double h00_im, int signal_band_limit, double* f_rec);
+
 #ifdef __cplusplus
 }
 #endif

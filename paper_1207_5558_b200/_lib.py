@@ -38,6 +38,7 @@ EXPORTS = [
     "slsht_cuda_kernel_time",
     "slsht_cuda_delta_tables",
     "slsht_cuda_modulated",
+    "slsht_cuda_inverse",
 ]
 
 
@@ -107,5 +108,8 @@ def load() -> C.CDLL:
     lib.slsht_cuda_delta_tables.restype = C.c_int
     lib.slsht_cuda_modulated.argtypes = [C.c_void_p, C.c_void_p, C.c_int, _ip, _ip, _dp]
     lib.slsht_cuda_modulated.restype = C.c_int
+    lib.slsht_cuda_inverse.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                                       C.c_double, C.c_int, C.c_void_p]
+    lib.slsht_cuda_inverse.restype = C.c_int
     _lib = lib
     return lib

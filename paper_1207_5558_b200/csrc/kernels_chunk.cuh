@@ -277,4 +277,33 @@ __global__ void k_digest(const CompRec* __restrict__ comps, int count, int n_col
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Inversion from the digests (transform.cpp:469-544): f_rec(l, m) = integral(l, m) /
+// (sqrt(16 pi^3) h00), the integral being digest fields 6-7 (integrate_volume). With
+// fill_negative, m < 0 comes from (-1)^m conj of (l, -m) (InverseAccumulator::finish).
+__global__ void k_inverse(const double* __restrict__ digest, int L, int fill_negative,
+                          double h00_re, double h00_im, double* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (L + 1) * (L + 1)) return;
+  int l = (int)sqrt((double)idx);
+  while (l * l > idx) --l;
+  while ((l + 1) * (l + 1) <= idx) ++l;
+  const int m = idx - l * l - l;
+  const bool mirror = fill_negative && m < 0;
+  const int src = mirror ? l * l + l - m : idx;
+  const double ir = digest[(size_t)src * 8 + 6], ii = digest[(size_t)src * 8 + 7];
+  // (ir + i ii) / (s h00), s = sqrt(16 pi^3), as complex division
+  const double s = sqrt(16.0 * kPi * kPi * kPi);
+  const double dr = s * h00_re, di = s * h00_im;
+  const double den = dr * dr + di * di;
+  double qr = (ir * dr + ii * di) / den, qi = (ii * dr - ir * di) / den;
+  if (mirror) {  // (-1)^m conj
+    const double sg = (m & 1) ? -1.0 : 1.0;
+    qr = sg * qr;
+    qi = -(sg * qi);
+  }
+  out[2 * (size_t)idx] = qr;
+  out[2 * (size_t)idx + 1] = qi;
+}
+
 }  // namespace slsht_cuda

@@ -930,11 +930,10 @@ const char* slsht_cuda_last_error(const slsht_cuda_plan* p) {
   return p ? p->last_error.c_str() : g_create_error.c_str();
 }
 
-int slsht_cuda_forward_device(slsht_cuda_plan* p, const double* f, const double* h,
-                              int inputs_on_device, double* digests, int digests_on_device,
-                              int synchronize) {
-  if (!p) return SLSHT_ERR_VALIDATION;
-  return guarded(p, [&] {
+void run_forward_device(slsht_cuda_plan* p, const double* f, const double* h,
+                        int inputs_on_device, double* digests, int digests_on_device,
+                        int synchronize) {
+  {
     if (!synchronize && digests && !digests_on_device)
       throw Status{SLSHT_ERR_VALIDATION, "asynchronous forward needs device digests"};
     p->launches = 0;
@@ -975,6 +974,15 @@ int slsht_cuda_forward_device(slsht_cuda_plan* p, const double* f, const double*
     }
     if (digests) copy_digests(p, digests, digests_on_device != 0);
     if (synchronize) check_numeric(p);
+  }
+}
+
+int slsht_cuda_forward_device(slsht_cuda_plan* p, const double* f, const double* h,
+                              int inputs_on_device, double* digests, int digests_on_device,
+                              int synchronize) {
+  if (!p) return SLSHT_ERR_VALIDATION;
+  return guarded(p, [&] {
+    run_forward_device(p, f, h, inputs_on_device, digests, digests_on_device, synchronize);
   });
 }
 
@@ -1147,6 +1155,33 @@ int slsht_cuda_delta_tables(int device, int L, double* out) {
     g_create_error = e.msg;
     return SLSHT_ERR_DEVICE;
   }
+}
+
+int slsht_cuda_inverse(slsht_cuda_plan* p, const double* f, const double* h, double h00_re,
+                       double h00_im, int signal_band_limit, double* f_rec) {
+  if (!p) return SLSHT_ERR_VALIDATION;
+  return guarded(p, [&] {
+    if (std::hypot(h00_re, h00_im) <= 1e-10)  // transform.cpp:513-514
+      throw Status{SLSHT_ERR_NUMERIC, "window DC component too small for inversion"};
+    if (signal_band_limit < 0 || p->l_begin > 0 || p->l_end <= signal_band_limit)
+      throw Status{SLSHT_ERR_VALIDATION, "distribution lacks components up to L_f"};
+    if (!f_rec) throw Status{SLSHT_ERR_VALIDATION, "null output"};
+    const int rows = coeff_count(signal_band_limit);
+    double* d_rec = dalloc<double>((size_t)2 * rows);
+    try {
+      run_forward_device(p, f, h, 0, nullptr, 0, 0);
+      k_inverse<<<(rows + 127) / 128, 128, 0, p->stream>>>(
+          p->d_digest, signal_band_limit, p->real_mode && !p->emit_neg, h00_re, h00_im, d_rec);
+      CKL();
+      CK(cudaMemcpyAsync(f_rec, d_rec, sizeof(double) * 2 * rows, cudaMemcpyDeviceToHost,
+                         p->stream));
+      check_numeric(p);
+    } catch (...) {
+      cudaFree(d_rec);
+      throw;
+    }
+    CK(cudaFree(d_rec));
+  });
 }
 
 int slsht_cuda_modulated(slsht_cuda_plan* p, const double* f, int count, const int* l,

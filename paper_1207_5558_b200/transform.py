@@ -210,6 +210,19 @@ class Plan:
         _raise(rc, self.handle)
         return dig, {k: vols[i] for i, k in enumerate(lm)}
 
+    def inverse(self, f: np.ndarray, h: np.ndarray, h00: complex,
+                signal_band_limit: int) -> np.ndarray:
+        """inverse_slsht(forward_fast(f, h), h00, L) (transform.cpp:469-544) on the device: the
+        forward's digest epilogue already holds every integrate_volume; returns f_rec."""
+        f = np.ascontiguousarray(f, np.complex128)
+        h = np.ascontiguousarray(h, np.complex128)
+        out = np.zeros(coeff_count(signal_band_limit), np.complex128)
+        rc = self.lib.slsht_cuda_inverse(self.handle, _dptr(f), _dptr(h), float(np.real(h00)),
+                                         float(np.imag(h00)), int(signal_band_limit),
+                                         _dptr(out))
+        _raise(rc, self.handle)
+        return out
+
     def forward_sink(self, f: np.ndarray, h: np.ndarray, sink) -> None:
         """Stream every emitted component to sink(l, m, volume) (volume valid during the call)."""
         f = np.ascontiguousarray(f, np.complex128)
