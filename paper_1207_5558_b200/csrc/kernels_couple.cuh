@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(NTHR, MINB) k_couple(const CoupleParams P) {
   constexpr int WT = MG * NG;       // 8x8 warp tiles
   constexpr int QS = (NTHR / 32) / WT;  // q split across warps
   constexpr int PAIRS = MT * NT;    // (comp, col) transforms per CTA
-  constexpr int D = 65536 / (NTHR * MINB) < 100 ? 4 : (65536 / (NTHR * MINB) >= 200 ? 24 : 8);  // register prefetch depth (k-steps)
+  constexpr int D = 65536 / (NTHR * MINB) < 100 ? 4 : (65536 / (NTHR * MINB) >= 200 ? 24 : 12);  // register prefetch depth (k-steps)
   static_assert((NTHR / 32) % WT == 0, "warp tiles must divide the warps");
   static_assert(NTHR % PAIRS == 0, "pairs must divide the block");
   extern __shared__ __align__(16) unsigned char smem_raw[];
