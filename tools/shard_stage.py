@@ -18,7 +18,7 @@ fd = torch.from_numpy(np.ascontiguousarray(f).view(np.float64)).to(dev)
 hd = torch.from_numpy(np.ascontiguousarray(h).view(np.float64)).to(dev)
 dig = torch.zeros((S.coeff_count(cfg.L_g), 8), dtype=torch.float64, device=dev)
 with S.Plan(cfg.L_f, cfg.L_h, real_mode=cfg.real_mode, l_begin=l0, l_end=l1,
-            materialize=False, ring_bytes=16384 << 20) as p:
+            materialize=False, ring_bytes=int(os.environ.get("RING_MB", "16384")) << 20) as p:
     p.forward_device(fd.data_ptr(), hd.data_ptr(), inputs_on_device=True,
                      digests_ptr=dig.data_ptr(), digests_on_device=True)
     p.set_profiling(True)
