@@ -6,7 +6,10 @@
 //  * the streaming contract: every component once, sink == materialized (test_transform.cpp:331-348);
 //  * the reference's InverseAccumulator consuming the shim's stream: acceptance criterion 1
 //    (acceptance_main.cpp:87-107, error < 1e-9);
-//  * ValidationError for lmax > L_f + L_h (transform.cpp:250-252).
+//  * ValidationError for lmax > L_f + L_h (transform.cpp:250-252);
+//  * the CLI's `forward --engine fast` path (cli.cpp:220-224): the reference's
+//    io::DistributionWriter as the sink, read back with io::read_component (SURVEY 8(f)
+//    next-2: host sink delivery and on-disk format through the drop-in).
 // Prints one PASS/FAIL line per check; exit status 0 iff all pass.
 #include <cmath>
 #include <complex>
@@ -16,7 +19,10 @@
 #include <random>
 #include <vector>
 
+#include <filesystem>
+
 #include "slsht/errors.hpp"
+#include "slsht/io.hpp"
 #include "slsht/signals.hpp"
 #include "slsht/transform.hpp"
 #include "slsht/window.hpp"
@@ -129,6 +135,41 @@ int main() {
       threw = true;
     }
     report(threw, "lmax > L_f + L_h throws ValidationError", threw ? 0.0 : 1.0, 0.0);
+  }
+  {
+    // cli.cpp:220-224 with the drop-in: DistributionWriter sink, files read back
+    const SphCoeffs f = random_coeffs(12, 41, true);
+    const Window win = eigenfunction_window(
+        {std::numbers::pi / 5.0, std::numbers::pi / 5.0 + std::numbers::pi / 200.0}, 6, 3);
+    const int top = 12 + 6;
+    const std::filesystem::path dir =
+        std::filesystem::temp_directory_path() / "slsht_shim_writer_test";
+    std::filesystem::remove_all(dir);
+    {
+      io::DistributionWriter writer(dir, 12, 6, top, true);
+      ForwardOptions opts;
+      opts.lmax = top;
+      forward_fast(f, win.coeffs, writer.sink(), opts);
+      writer.finalize();
+    }
+    const io::DistributionManifest man = io::read_manifest(dir);
+    ForwardOptions opts;
+    opts.lmax = top;
+    const SlshtDistribution ref = reference_forward_fast(f, win.coeffs, opts);
+    double num = 0.0, den = 0.0;
+    bool complete = man.components.size() == static_cast<std::size_t>(coeff_count(top));
+    for (const auto& [l, m] : man.components) {
+      const So3Volume v = io::read_component(dir, man, l, m);
+      const So3Volume& r = ref.component(l, m);
+      for (std::size_t i = 0; i < r.values.size(); ++i) {
+        num = std::max(num, std::abs(v.values[i] - r.values[i]));
+        den = std::max(den, std::abs(r.values[i]));
+      }
+    }
+    std::filesystem::remove_all(dir);
+    const double rel = complete ? num / den : 1.0;
+    report(complete && rel < 1e-12, "CLI path: DistributionWriter sink, files vs reference", rel,
+           1e-12);
   }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ALL PASSED", failures);
   return failures ? 1 : 0;
