@@ -142,6 +142,16 @@ int slsht_cuda_modulated(slsht_cuda_plan* plan, const double* f, int count, cons
 int slsht_cuda_inverse(slsht_cuda_plan* plan, const double* f, const double* h,
                        double h00_re, double h00_im, int signal_band_limit, double* f_rec);
 
+/* Slepian window (window.cpp:44-198: concentration_matrix + eigenfunction_window): the
+ * dominant eigenfunction of the concentration kernel of the elliptical region (foci at
+ * colatitude theta_c on phi = 0, pi; semi-major arc a) at band limit L, by mask quadrature on
+ * S_{oversample L} and the reference's power iteration, on `device`.
+ * coeffs: coeff_count(L) complex (host), unit norm, real-signal symmetric; lambda: the
+ * concentration ratio. Errors as the reference (ValidationError / NumericError codes); the
+ * message is slsht_cuda_last_error(NULL). */
+int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int band_limit,
+                                    int oversample, double* coeffs, double* lambda);
+
 #ifdef __cplusplus
 }
 #endif

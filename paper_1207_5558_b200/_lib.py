@@ -39,6 +39,7 @@ EXPORTS = [
     "slsht_cuda_delta_tables",
     "slsht_cuda_modulated",
     "slsht_cuda_inverse",
+    "slsht_cuda_eigenfunction_window",
 ]
 
 
@@ -106,6 +107,9 @@ def load() -> C.CDLL:
     lib.slsht_cuda_kernel_time.restype = C.c_int
     lib.slsht_cuda_delta_tables.argtypes = [C.c_int, C.c_int, _dp]
     lib.slsht_cuda_delta_tables.restype = C.c_int
+    lib.slsht_cuda_eigenfunction_window.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int,
+                                                    C.c_int, C.c_void_p, _dp]
+    lib.slsht_cuda_eigenfunction_window.restype = C.c_int
     lib.slsht_cuda_modulated.argtypes = [C.c_void_p, C.c_void_p, C.c_int, _ip, _ip, _dp]
     lib.slsht_cuda_modulated.restype = C.c_int
     lib.slsht_cuda_inverse.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,

@@ -15,6 +15,7 @@
 #include "kernels_couple.cuh"
 #include "kernels_couple_ws.cuh"
 #include "kernels_couple_lines.cuh"
+#include "window_solver.cuh"
 #include "kernels_setup.cuh"
 #include "slsht_cuda.h"
 
@@ -1127,6 +1128,195 @@ int slsht_cuda_kernel_time(const slsht_cuda_plan* p, double* ms_out) {
   }
   *ms_out = ms;
   return SLSHT_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Slepian window (window.cpp:44-198) on the device; see window_solver.cuh.
+namespace {
+
+// theta_weights(N) (grids.cpp:76-92), the reference's serial k order: the same weights
+std::vector<double> host_theta_weights(int N) {
+  std::vector<double> w(N + 1);
+  for (int t = 0; t <= N; ++t) {
+    const double theta = kPi * (2 * t + 1) / (2 * N + 1);
+    double sr = 0.0, si = 0.0;
+    for (int k = -N; k <= N; ++k) {
+      const int mk = -k;
+      double wr = 0.0, wi = 0.0;
+      if (mk == 0) wr = 2.0;
+      else if (mk == 1) wi = kPi / 2.0;
+      else if (mk == -1) wi = -kPi / 2.0;
+      else if ((mk & 1) == 0) wr = 2.0 / (1.0 - (double)mk * mk);
+      if (wr == 0.0 && wi == 0.0) continue;
+      const double ck = std::cos(k * theta);
+      sr += wr * ck;
+      si += wi * ck;
+    }
+    if (std::fabs(si) >= 1e-12)
+      throw Status{SLSHT_ERR_NUMERIC, "theta weight imaginary residue exceeds 1e-12"};
+    w[t] = (t < N) ? 2.0 * sr / (2 * N + 1) : sr / (2 * N + 1);
+  }
+  return w;
+}
+
+double angular_distance(double t1, double p1, double t2, double p2) {
+  const double c = std::sin(t1) * std::sin(t2) * std::cos(p1 - p2) + std::cos(t1) * std::cos(t2);
+  return std::acos(std::min(1.0, std::max(-1.0, c)));
+}
+
+#define CB(x)                                                                        \
+  do {                                                                               \
+    const cublasStatus_t st_ = (x);                                                  \
+    if (st_ != CUBLAS_STATUS_SUCCESS)                                                \
+      throw Status{SLSHT_ERR_DEVICE, std::string(#x) + ": cuBLAS status " +           \
+                                         std::to_string((int)st_)};                  \
+  } while (0)
+
+}  // namespace
+
+int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int band_limit,
+                                    int oversample, double* coeffs, double* lambda_out) {
+  std::vector<void*> allocs;
+  cublasHandle_t hb = nullptr;
+  auto cleanup = [&]() {
+    if (hb) cublasDestroy(hb);
+    for (void* q : allocs) cudaFree(q);
+  };
+  try {
+    if (!(theta_c >= 0.0) || !(theta_c <= a) || !(a <= kPi / 2.0))  // window.cpp:28-33
+      throw Status{SLSHT_ERR_VALIDATION, "elliptical region requires 0 <= theta_c <= a <= pi/2"};
+    if (band_limit < 0) throw Status{SLSHT_ERR_VALIDATION, "band limit must be non-negative"};
+    if (oversample < 2) throw Status{SLSHT_ERR_VALIDATION, "oversample must be at least 2"};
+    if (!coeffs || !lambda_out) throw Status{SLSHT_ERR_VALIDATION, "null output"};
+    int dev_count = 0;
+    if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+      throw Status{SLSHT_ERR_DEVICE, "no CUDA device available (the engine has no CPU fallback)"};
+    CK(cudaSetDevice(device));
+    const int L = band_limit, dim = coeff_count(L), N = oversample * L;
+    const int n_phi = 2 * N + 1;
+    const std::vector<double> ring = host_theta_weights(N);
+    const double dphi = 2.0 * kPi / n_phi;
+    std::vector<double> st, sp, sw;  // mask samples (window.cpp:64-71)
+    for (int t = 0; t <= N; ++t) {
+      const double theta = kPi * (2 * t + 1) / (2 * N + 1);
+      for (int q = 0; q < n_phi; ++q) {
+        const double phi = 2.0 * kPi * q / n_phi;
+        const double d = angular_distance(theta, phi, theta_c, 0.0) +
+                         angular_distance(theta, phi, theta_c, kPi);
+        if (d <= 2.0 * a) {
+          st.push_back(theta);
+          sp.push_back(phi);
+          sw.push_back(ring[t] * dphi);
+        }
+      }
+    }
+    const int S = (int)st.size();
+    if (S < 10)
+      throw Status{SLSHT_ERR_VALIDATION,
+                   "region mask holds fewer than 10 grid samples; raise oversample or widen the "
+                   "region"};
+    auto dal = [&](size_t bytes) {
+      void* q = nullptr;
+      CK(cudaMalloc(&q, bytes));
+      allocs.push_back(q);
+      return q;
+    };
+    double* d_t = (double*)dal(sizeof(double) * S);
+    double* d_p = (double*)dal(sizeof(double) * S);
+    double* d_w = (double*)dal(sizeof(double) * S);
+    CK(cudaMemcpy(d_t, st.data(), sizeof(double) * S, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_p, sp.data(), sizeof(double) * S, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_w, sw.data(), sizeof(double) * S, cudaMemcpyHostToDevice));
+    double2* d_Y = (double2*)dal(sizeof(double2) * (size_t)S * dim);
+    double2* d_B = (double2*)dal(sizeof(double2) * (size_t)S * dim);
+    double2* d_K = (double2*)dal(sizeof(double2) * (size_t)dim * dim);
+    double2* d_v = (double2*)dal(sizeof(double2) * dim);
+    double2* d_x = (double2*)dal(sizeof(double2) * dim);
+    const int ny = S * (2 * L + 1);
+    k_window_y<<<(ny + 127) / 128, 128>>>(L, S, d_t, d_p, d_Y);
+    CKL();
+    const size_t nb = (size_t)S * dim;
+    k_window_scale<<<(unsigned)((nb + 255) / 256), 256>>>(dim, S, d_w, d_Y, d_B);
+    CKL();
+    CB(cublasCreate(&hb));
+    // row-major Y[s][c] is the column-major dim x S matrix A; K (row-major) = A B^H
+    // (column-major), B = A diag(w): K[r][c] = sum_s conj(Y[s][r]) w_s Y[s][c]
+    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+    CB(cublasZgemm(hb, CUBLAS_OP_N, CUBLAS_OP_C, dim, dim, S, &one,
+                   reinterpret_cast<const cuDoubleComplex*>(d_Y), dim,
+                   reinterpret_cast<const cuDoubleComplex*>(d_B), dim, &zero,
+                   reinterpret_cast<cuDoubleComplex*>(d_K), dim));
+    const size_t nk = (size_t)dim * dim;
+    k_window_symmetrize<<<(unsigned)((nk + 255) / 256), 256>>>(dim, d_K);
+    CKL();
+    // power iteration (window.cpp:129-157), v0 = e_(0,0)
+    std::vector<double2> v(dim, make_double2(0.0, 0.0));
+    v[0] = make_double2(1.0, 0.0);
+    CK(cudaMemcpy(d_v, v.data(), sizeof(double2) * dim, cudaMemcpyHostToDevice));
+    double lambda_prev = -1.0, lambda = 0.0;
+    bool converged = false;
+    for (int it = 0; it < 100000; ++it) {
+      // w = K v: K row-major is the column-major K^T
+      CB(cublasZgemv(hb, CUBLAS_OP_T, dim, dim, &one, reinterpret_cast<cuDoubleComplex*>(d_K),
+                     dim, reinterpret_cast<cuDoubleComplex*>(d_v), 1, &zero,
+                     reinterpret_cast<cuDoubleComplex*>(d_x), 1));
+      cuDoubleComplex rq;
+      double nw = 0.0;
+      CB(cublasZdotc(hb, dim, reinterpret_cast<cuDoubleComplex*>(d_v), 1,
+                     reinterpret_cast<cuDoubleComplex*>(d_x), 1, &rq));
+      CB(cublasDznrm2(hb, dim, reinterpret_cast<cuDoubleComplex*>(d_x), 1, &nw));
+      lambda = cuCreal(rq);
+      if (nw == 0.0) throw Status{SLSHT_ERR_NUMERIC, "power iteration collapsed to zero"};
+      const double inv = 1.0 / nw;
+      CB(cublasZdscal(hb, dim, &inv, reinterpret_cast<cuDoubleComplex*>(d_x), 1));
+      std::swap(d_v, d_x);
+      if (it > 0 && std::fabs(lambda - lambda_prev) <= 1e-12 * std::fabs(lambda)) {
+        converged = true;
+        break;
+      }
+      lambda_prev = lambda;
+    }
+    if (!converged)
+      throw Status{SLSHT_ERR_NUMERIC, "power iteration did not converge within 1e5 steps"};
+    CK(cudaMemcpy(v.data(), d_v, sizeof(double2) * dim, cudaMemcpyDeviceToHost));
+    // north-pole phase, exact conjugate symmetry, unit norm (window.cpp:159-196)
+    std::vector<std::complex<double>> z(dim);
+    for (int i = 0; i < dim; ++i) z[i] = {v[i].x, v[i].y};
+    std::complex<double> pole{0.0, 0.0};
+    for (int l = 0; l <= L; ++l) pole += z[l * l + l] * std::sqrt((2.0 * l + 1.0) / (4.0 * kPi));
+    if (std::abs(pole) > 0.0) {
+      const std::complex<double> phase = std::conj(pole) / std::abs(pole);
+      for (auto& x : z) x *= phase;
+    }
+    std::vector<std::complex<double>> c(dim);
+    for (int l = 0; l <= L; ++l) {
+      c[l * l + l] = {z[l * l + l].real(), 0.0};
+      for (int m = 1; m <= l; ++m) {
+        const double sign = (m & 1) ? -1.0 : 1.0;
+        const std::complex<double> sym = 0.5 * (z[l * l + l + m] + sign * std::conj(z[l * l + l - m]));
+        c[l * l + l + m] = sym;
+        c[l * l + l - m] = sign * std::conj(sym);
+      }
+    }
+    double norm = 0.0;
+    for (const auto& x : c) norm += std::norm(x);
+    norm = std::sqrt(norm);
+    if (norm == 0.0) throw Status{SLSHT_ERR_NUMERIC, "eigenfunction window is zero"};
+    for (auto& x : c) x /= norm;
+    if (std::abs(c[0]) < 1e-10)
+      throw Status{SLSHT_ERR_NUMERIC, "window DC component vanishes; inversion would be impossible"};
+    for (int i = 0; i < dim; ++i) {
+      coeffs[2 * i] = c[i].real();
+      coeffs[2 * i + 1] = c[i].imag();
+    }
+    *lambda_out = lambda;
+    cleanup();
+    return SLSHT_OK;
+  } catch (const Status& st) {
+    cleanup();
+    g_create_error = st.msg;
+    return st.code;
+  }
 }
 
 int slsht_cuda_delta_tables(int device, int L, double* out) {

@@ -291,6 +291,19 @@ def delta_tables(band_limit: int, device: int = 0) -> np.ndarray:
     return out
 
 
+def eigenfunction_window(theta_c: float, a: float, band_limit: int, oversample: int = 4,
+                         device: int = 0) -> tuple[np.ndarray, float]:
+    """eigenfunction_window(EllipticalRegion{theta_c, a}, L, oversample) (window.cpp:126-198) on
+    the device: (unit-norm coefficients, concentration ratio lambda)."""
+    lib = L.load()
+    out = np.zeros(coeff_count(band_limit), np.complex128)
+    lam = C.c_double(0.0)
+    rc = lib.slsht_cuda_eigenfunction_window(device, float(theta_c), float(a), int(band_limit),
+                                             int(oversample), out.ctypes.data, C.byref(lam))
+    _raise(rc, None)
+    return out, float(lam.value)
+
+
 def modulated_sht(f: SphCoeffs, lm: list[tuple[int, int]], window_band_limit: int,
                   device: int = 0) -> np.ndarray:
     """ModulatedSht::compute for several (l, m): [len(lm), coeff_count(L_h)] complex."""
