@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1192,6 +1193,15 @@ int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int ba
     if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
       throw Status{SLSHT_ERR_DEVICE, "no CUDA device available (the engine has no CPU fallback)"};
     CK(cudaSetDevice(device));
+    const bool prof = std::getenv("SLSHT_CUDA_PROFILE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t0 = now();
+    auto lap = [&](const char* what) {
+      if (!prof) return;
+      CK(cudaDeviceSynchronize());
+      fprintf(stderr, "window: %-24s %.3f s\n", what,
+              std::chrono::duration<double>(now() - t0).count());
+    };
     const int L = band_limit, dim = coeff_count(L), N = oversample * L;
     const int n_phi = 2 * N + 1;
     const std::vector<double> ring = host_theta_weights(N);
@@ -1211,6 +1221,7 @@ int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int ba
       }
     }
     const int S = (int)st.size();
+    lap("mask (host)");
     if (S < 10)
       throw Status{SLSHT_ERR_VALIDATION,
                    "region mask holds fewer than 10 grid samples; raise oversample or widen the "
@@ -1249,6 +1260,7 @@ int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int ba
     const size_t nk = (size_t)dim * dim;
     k_window_symmetrize<<<(unsigned)((nk + 255) / 256), 256>>>(dim, d_K);
     CKL();
+    lap("Y, K (device)");
     // power iteration (window.cpp:129-157), v0 = e_(0,0)
     std::vector<double2> v(dim, make_double2(0.0, 0.0));
     v[0] = make_double2(1.0, 0.0);
@@ -1278,6 +1290,7 @@ int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int ba
     }
     if (!converged)
       throw Status{SLSHT_ERR_NUMERIC, "power iteration did not converge within 1e5 steps"};
+    lap("power iteration");
     CK(cudaMemcpy(v.data(), d_v, sizeof(double2) * dim, cudaMemcpyDeviceToHost));
     // north-pole phase, exact conjugate symmetry, unit norm (window.cpp:159-196)
     std::vector<std::complex<double>> z(dim);
