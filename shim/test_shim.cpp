@@ -7,6 +7,8 @@
 //  * the reference's InverseAccumulator consuming the shim's stream: acceptance criterion 1
 //    (acceptance_main.cpp:87-107, error < 1e-9);
 //  * ValidationError for lmax > L_f + L_h (transform.cpp:250-252);
+//  * eigenfunction_window through the shim (window.cpp:126-198 on the device) against the
+//    reference's CPU solver;
 //  * the CLI's `forward --engine fast` path (cli.cpp:220-224): the reference's
 //    io::DistributionWriter as the sink, read back with io::read_component (SURVEY 8(f)
 //    next-2: host sink delivery and on-disk format through the drop-in).
@@ -33,6 +35,9 @@ void reference_forward_fast(const SphCoeffs& f, const SphCoeffs& h, const Compon
                             const ForwardOptions& opts);
 SlshtDistribution reference_forward_fast(const SphCoeffs& f, const SphCoeffs& h,
                                          const ForwardOptions& opts);
+// the reference's CPU window solver, renamed at compile time (see Makefile)
+Window reference_eigenfunction_window(const EllipticalRegion& region, int band_limit,
+                                      int oversample);
 }  // namespace slsht
 
 using namespace slsht;
@@ -170,6 +175,30 @@ int main() {
     const double rel = complete ? num / den : 1.0;
     report(complete && rel < 1e-12, "CLI path: DistributionWriter sink, files vs reference", rel,
            1e-12);
+  }
+  {
+    // eigenfunction_window: device solver (shim) vs the reference's CPU solver
+    double worst = 0.0, dl = 0.0;
+    const EllipticalRegion regions[] = {{std::numbers::pi / 9.0, std::numbers::pi / 6.0},
+                                        {0.3, 0.7}};
+    const int bls[] = {16, 6};
+    for (int i = 0; i < 2; ++i) {
+      const Window a = eigenfunction_window(regions[i], bls[i], 4);
+      const Window b = reference_eigenfunction_window(regions[i], bls[i], 4);
+      for (std::size_t k = 0; k < a.coeffs.data.size(); ++k)
+        worst = std::max(worst, std::abs(a.coeffs.data[k] - b.coeffs.data[k]));
+      dl = std::max(dl, std::abs(a.lambda - b.lambda));
+    }
+    report(worst < 1e-9 && dl < 1e-12, "eigenfunction_window (device) vs reference solver", worst,
+           1e-9);
+    bool threw = false;
+    try {
+      eigenfunction_window({0.8, 0.5}, 4, 4);
+    } catch (const ValidationError&) {
+      threw = true;
+    }
+    report(threw, "eigenfunction_window: theta_c > a throws ValidationError", threw ? 0.0 : 1.0,
+           0.0);
   }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ALL PASSED", failures);
   return failures ? 1 : 0;
