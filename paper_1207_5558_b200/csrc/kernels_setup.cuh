@@ -313,14 +313,16 @@ __host__ __device__ __forceinline__ size_t wtile_index(int c, int col, int NPQ, 
 
 __global__ void k_wtab(int L, const double* __restrict__ h, const double* __restrict__ dtab,
                        const double2* __restrict__ rou, const int* __restrict__ pq_q,
-                       int tile_nt, int ncol_pad, double2* __restrict__ W) {
+                       int tile_nt, int ncol_pad, const int* __restrict__ wrow,
+                       double2* __restrict__ W) {
   const int n = 2 * L + 1, nb = L + 1, ncol = n * nb;
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   const int NPQ = (L + 1) * (L + 1);
   if (col >= ncol_pad) return;
   if (col >= ncol) {
-    W[wtile_index(c, col, NPQ, tile_nt)] = make_double2(0.0, 0.0);
+    W[wrow ? (size_t)wrow[c] * ncol_pad + col : wtile_index(c, col, NPQ, tile_nt)] =
+        make_double2(0.0, 0.0);
     return;
   }
   const int q = pq_q[2 * c], p = pq_q[2 * c + 1];
@@ -339,7 +341,10 @@ __global__ void k_wtab(int L, const double* __restrict__ h, const double* __rest
     ar += tr * z.x - ti * z.y;
     ai += tr * z.y + ti * z.x;
   }
-  const size_t dst = tile_nt ? wtile_index(c, col, NPQ, tile_nt) : (size_t)c * ncol + col;
+  // wrow: the two-pass GEMM's q-padded row layout with row stride ncol_pad
+  const size_t dst = wrow      ? (size_t)wrow[c] * ncol_pad + col
+                     : tile_nt ? wtile_index(c, col, NPQ, tile_nt)
+                               : (size_t)c * ncol + col;
   W[dst] = make_double2(ar, ai);
 }
 

@@ -16,6 +16,7 @@
 #include "kernels_couple.cuh"
 #include "kernels_couple_ws.cuh"
 #include "kernels_couple_lines.cuh"
+#include "kernels_twopass.cuh"
 #include "window_solver.cuh"
 #include "kernels_setup.cuh"
 #include "slsht_cuda.h"
@@ -111,6 +112,13 @@ struct slsht_cuda_plan {
   int lines_nseg_dig = 1;  // digest segments per group (fixed per n: the digests do not depend
                            // on the execution split, the chunking or the sharding)
   int lines_urb[136] = {};
+  bool use_tp = false;     // two-pass coupling: k_tgemm (T to HBM) + k_qfft (n = 49, 65, 129)
+  int tp_KP = 0;           //   q-padded (p, q) rows
+  int tp_ncolp = 0;        //   padded column stride of W and T
+  int tp_ntiles = 0;       //   k_qfft column tiles (digest partials per component)
+  int tp_threads = 0;
+  size_t tp_gemm_smem = 0, tp_fft_smem = 0;
+  void (*tp_fft)(QfParams) = nullptr;
   int* d_ubase = nullptr;  // stage-tiled U layout (ws path): per (p, q) row block offset
   int* d_ustr = nullptr;   //   and row stride
   int ct_fast = 0;
@@ -150,6 +158,9 @@ struct slsht_cuda_plan {
   MTile* d_tiles = nullptr;
   double* d_A = nullptr;
   double2* d_U = nullptr;
+  double2* d_T = nullptr;   // two-pass: T of one chunk
+  short* d_qend = nullptr;  // two-pass: per k-step, the T row it completes (or -1)
+  int* d_wrow = nullptr;    // two-pass: W row of every (p, q)
   double2* d_out = nullptr;
   double* d_partials = nullptr;
   double* d_digest = nullptr;
@@ -170,6 +181,9 @@ namespace {
 void free_plan(slsht_cuda_plan* p) {
   if (!p) return;
   cudaFree(p->d_f);
+  cudaFree(p->d_T);
+  cudaFree(p->d_qend);
+  cudaFree(p->d_wrow);
   cudaFree(p->d_h);
   cudaFree(p->d_ncos);
   cudaFree(p->d_nsin);
@@ -279,6 +293,17 @@ bool ws_kernel(int n, WsKernel& k) {
   }
 }
 
+// Two-pass coupling (kernels_twopass.cuh): the k_qfft instantiation per BASELINE length.
+bool tp_kernel(int n, void (*&fn)(QfParams), int& threads) {
+  switch (n) {
+    case 65: fn = k_qfft<65, 128, 4>; break;
+    case 129: fn = k_qfft<129, 128, 2>; break;
+    default: return false;
+  }
+  threads = 128;
+  return true;
+}
+
 int couple_threads(int n) {
   switch (n) {
     case 17:
@@ -315,6 +340,14 @@ void build_plan(slsht_cuda_plan* p) {
   p->n_nodes = p->N + 1;
   p->ldA = (p->n_nodes + MG_K - 1) / MG_K * MG_K;
   p->vol = (long long)p->n * p->n * p->nb;
+  // two-pass coupling for the long transforms unless SLSHT_CUDA_TWO_PASS=0 (the single-pass
+  // k_couple then runs); n = 33 keeps its line kernel, n = 17 its warp-specialized kernel
+  {
+    const char* e = std::getenv("SLSHT_CUDA_TWO_PASS");
+    p->use_tp = !(e && e[0] == '0') && tp_kernel(p->n, p->tp_fft, p->tp_threads);
+    p->tp_ncolp = (p->ncol + TG_BN - 1) / TG_BN * TG_BN;
+    p->tp_ntiles = (p->ncol + QF_NT - 1) / QF_NT;
+  }
   // ---- component list: orders m (all or m >= 0 in real mode), degrees in the shard
   for (int m = p->real_mode ? 0 : -p->lmax; m <= p->lmax; ++m) {
     const int lo = std::max(std::abs(m), p->l_begin), hi = std::min(p->lmax, p->l_end - 1);
@@ -330,6 +363,11 @@ void build_plan(slsht_cuda_plan* p) {
     p->slot_base = (long long)p->l_begin * p->l_begin;
     p->n_slots = (long long)p->l_end * p->l_end - p->slot_base;
     p->max_chunk = (int)std::min<long long>(std::max<long long>(total, 1), 16384);
+    if (p->use_tp) {  // the chunk's T buffer stays below 4 GiB
+      const long long tcomp = (long long)p->n * p->tp_ncolp * 16;
+      p->max_chunk = (int)std::max<long long>(
+          TG_BM, std::min<long long>(p->max_chunk, (4LL << 30) / tcomp / TG_BM * TG_BM));
+    }
   } else {
     long long ring = d.ring_bytes > 0 ? d.ring_bytes : (1LL << 31);
     const int per = p->mirror ? 2 : 1;
@@ -337,6 +375,23 @@ void build_plan(slsht_cuda_plan* p) {
     ch = std::max<long long>(8, ch / 8 * 8);
     ch = std::min<long long>(ch, 16384);
     ch = std::min<long long>(ch, std::max<long long>(8, (total + 7) / 8 * 8));
+    if (p->use_tp && ch >= 2 * TG_BM) {
+      // whole 64-component GEMM blocks, as many as give full waves of k_tgemm CTAs
+      int sms = 148;
+      if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device) != cudaSuccess)
+        sms = 148;
+      const long long nct = p->tp_ncolp / TG_BN, bmax = ch / TG_BM;
+      long long best_b = bmax;
+      double best = 0.0;
+      for (long long b = bmax; b >= (bmax + 1) / 2; --b) {
+        const double eff = (double)(b * nct) / (double)(((b * nct + sms - 1) / sms) * sms);
+        if (eff > best + 0.01) {
+          best = eff;
+          best_b = b;
+        }
+      }
+      ch = best_b * TG_BM;
+    }
     p->max_chunk = (int)ch;
     p->n_slots = 2LL * per * ch;
   }
@@ -376,7 +431,7 @@ void build_plan(slsht_cuda_plan* p) {
     p->ws_stages.js[++cnt] = p->n;
     p->ws_stages.count = cnt;
   }
-  p->n_col_tiles = (p->ncol + 8 * p->NG - 1) / (8 * p->NG);
+  p->n_col_tiles = p->use_tp ? p->tp_ntiles : (p->ncol + 8 * p->NG - 1) / (8 * p->NG);
   const char* prof = std::getenv("SLSHT_CUDA_PROFILE");
   p->profile = prof && prof[0] == '1';
 
@@ -454,6 +509,32 @@ void build_plan(slsht_cuda_plan* p) {
         ustr[c] = p->lines_upad;
       }
     p->ws_stages.group_elems = 8LL * p->lines_upad;
+  }
+  // ---- two-pass GEMM layout: every q's rows padded with zeros to whole k-steps of 4, the
+  // same row positions in U (per component, stride KP) and W (stride ncolp); qend marks the
+  // k-step that completes each q, with the T row (q mod n) it is stored to
+  std::vector<int> wrow;
+  std::vector<short> qend;
+  if (p->use_tp) {
+    int rows_pad = 0;
+    wrow.assign(p->NPQ, 0);
+    std::vector<int> urb(p->n + 1, 0);
+    for (int jq = 0; jq < p->n; ++jq) {
+      urb[jq] = rows_pad;
+      rows_pad += (qoff[jq + 1] - qoff[jq] + 3) / 4 * 4;
+    }
+    urb[p->n] = rows_pad;
+    p->tp_KP = rows_pad;
+    qend.assign(rows_pad / 4, (short)-1);
+    for (int jq = 0; jq < p->n; ++jq) {
+      for (int c = qoff[jq]; c < qoff[jq + 1]; ++c) {
+        ubase[c] = urb[jq] + (c - qoff[jq]);
+        ustr[c] = 0;
+        wrow[c] = ubase[c];
+      }
+      qend[urb[jq + 1] / 4 - 1] = (short)(jq >= L ? jq - L : jq + L + 1);
+    }
+    p->ws_stages.group_elems = rows_pad;
   }
   // ---- alpha-axis FFT plan: roots of unity, DIF stages, output permutation, phase shift
   const int n = p->n;
@@ -551,7 +632,14 @@ void build_plan(slsht_cuda_plan* p) {
   p->d_dtab = dalloc<double>(dsz * p->nb);
   const int tile_nt_alloc = p->use_lines ? 8 : (p->use_ws ? p->ws.NT : 0);
   const size_t ncol_pad = tile_nt_alloc ? (size_t)p->n_col_tiles * tile_nt_alloc : (size_t)p->ncol;
-  p->d_W = dalloc<double2>((size_t)p->NPQ * ncol_pad);
+  if (p->use_tp) {
+    p->d_W = dalloc<double2>((size_t)p->tp_KP * p->tp_ncolp);
+    CK(cudaMemsetAsync(p->d_W, 0, (size_t)p->tp_KP * p->tp_ncolp * 16, s));  // padding rows
+    p->d_wrow = dupload(wrow, s);
+    p->d_qend = dupload(qend, s);
+  } else {
+    p->d_W = dalloc<double2>((size_t)p->NPQ * ncol_pad);
+  }
   p->ct_fast = (size_t)p->NPQ * ncol_pad * 16 < (48u << 20);
   p->d_ubase = dupload(ubase, s);
   p->d_ustr = dupload(ustr, s);
@@ -566,7 +654,10 @@ void build_plan(slsht_cuda_plan* p) {
   p->d_segs = dupload(p->segs, s);
   p->d_tiles = dupload(p->tiles, s);
   p->d_A = dalloc<double>((size_t)p->max_chunk * p->ldA);
-  if (p->use_ws || p->use_lines) {
+  if (p->use_tp) {
+    p->d_U = dalloc<double2>((size_t)p->max_chunk * p->tp_KP);
+    CK(cudaMemsetAsync(p->d_U, 0, (size_t)p->max_chunk * p->tp_KP * 16, s));  // padding rows
+  } else if (p->use_ws || p->use_lines) {
     const int gmt = p->use_lines ? 8 : p->ws.MT;
     const size_t groups = (size_t)(p->max_chunk + gmt - 1) / gmt;
     p->d_U = dalloc<double2>(groups * (size_t)p->ws_stages.group_elems);
@@ -577,10 +668,12 @@ void build_plan(slsht_cuda_plan* p) {
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   const size_t out_bytes = (size_t)p->n_slots * vol_bytes;
-  if (out_bytes + (64u << 20) > free_b)
+  const size_t t_bytes = p->use_tp ? (size_t)p->max_chunk * p->n * p->tp_ncolp * 16 : 0;
+  if (out_bytes + t_bytes + (64u << 20) > free_b)
     throw Status{SLSHT_ERR_VALIDATION,
                  "device output buffer does not fit in HBM (use the streaming ring mode)"};
   p->d_out = dalloc<double2>((size_t)p->n_slots * p->vol);
+  if (p->use_tp) p->d_T = dalloc<double2>(t_bytes / 16);
   p->d_partials = dalloc<double>((size_t)p->max_chunk * p->n_col_tiles * 8);
   p->digest_rows = coeff_count(p->lmax);
   p->d_digest = dalloc<double>((size_t)p->digest_rows * 8);
@@ -603,6 +696,14 @@ void build_plan(slsht_cuda_plan* p) {
   if (p->use_lines) {
     CK(cudaFuncSetAttribute(p->lines_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)p->couple_smem));
+  } else if (p->use_tp) {
+    p->tp_gemm_smem = tgemm_smem_bytes(p->tp_KP);
+    p->tp_fft_smem = qfft_smem_bytes(p->n);
+    p->couple_smem = std::max(p->tp_gemm_smem, p->tp_fft_smem);
+    CK(cudaFuncSetAttribute(k_tgemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)p->tp_gemm_smem));
+    CK(cudaFuncSetAttribute(p->tp_fft, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)p->tp_fft_smem));
   } else if (p->use_ws) {
     p->couple_smem = p->ws.smem;
     CK(cudaFuncSetAttribute(p->ws.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -709,9 +810,10 @@ void run_setup(slsht_cuda_plan* p) {
   k_dtab<<<dim3((wmax + 255) / 256, L + 1), 256, 0, a>>>(L, p->d_delta, p->d_rou, p->d_dtab);
   CKL();
   const int tile_nt = p->use_lines ? 8 : (p->use_ws ? p->ws.NT : 0);
-  const int ncol_pad = tile_nt ? p->n_col_tiles * tile_nt : p->ncol;
-  k_wtab<<<dim3((ncol_pad + 127) / 128, p->NPQ), 128, 0, a>>>(L, p->d_h, p->d_dtab, p->d_rou,
-                                                             p->d_pq, tile_nt, ncol_pad, p->d_W);
+  const int ncol_pad = p->use_tp ? p->tp_ncolp : (tile_nt ? p->n_col_tiles * tile_nt : p->ncol);
+  k_wtab<<<dim3((ncol_pad + 127) / 128, p->NPQ), 128, 0, a>>>(
+      L, p->d_h, p->d_dtab, p->d_rou, p->d_pq, tile_nt, ncol_pad, p->use_tp ? p->d_wrow : nullptr,
+      p->d_W);
   CKL();
   CK(cudaEventRecord(p->ev_wtab, a));
   p->wtab_pending = true;
@@ -730,7 +832,8 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   record(p, 1);
   k_modgemm<<<dim3(ch.ntile, (p->NPQ + MG_COLS - 1) / MG_COLS), 256, MG_SMEM, s>>>(
       p->d_tiles + ch.tile0, p->n_nodes, p->ldA, p->L_f, p->NPQ, p->d_A, p->d_itab, p->d_lamh,
-      p->d_pq, p->use_lines ? 8 : (p->use_ws ? p->ws.MT : 0), p->ws_stages.group_elems,
+      p->d_pq, p->use_lines ? 8 : (p->use_ws ? p->ws.MT : (p->use_tp ? 1 : 0)),
+      p->ws_stages.group_elems,
       p->d_ubase, p->d_ustr, p->d_U);
   CKL();
   join_aux(p);
@@ -758,6 +861,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   prm.betaw = p->d_betaw;
   prm.fft = p->fft;
   prm.generic_dft = p->generic_dft;
+  prm.group_major = std::getenv("SLSHT_CUDA_GROUP_MAJOR") != nullptr;
   const int MT = 8 * p->MG;
   if (p->use_lines) {
     LnParams lp{};
@@ -825,8 +929,39 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
       }
     }
 #endif
+  } else if (p->use_tp) {
+    TgParams tg{};
+    tg.U = p->d_U;
+    tg.W = p->d_W;
+    tg.T = p->d_T;
+    tg.qend = p->d_qend;
+    tg.count = ch.count;
+    tg.KP = p->tp_KP;
+    tg.ncolp = p->tp_ncolp;
+    tg.n = p->n;
+    k_tgemm<<<dim3((ch.count + TG_BM - 1) / TG_BM, p->tp_ncolp / TG_BN), TG_THREADS,
+              p->tp_gemm_smem, s>>>(tg);
+    CKL();
+    QfParams qf{};
+    qf.T = p->d_T;
+    qf.out = p->d_out;
+    qf.partials = p->d_partials;
+    qf.comps = comps;
+    qf.count = ch.count;
+    qf.n = p->n;
+    qf.ncol = p->ncol;
+    qf.ncolp = p->tp_ncolp;
+    qf.n_tiles = p->tp_ntiles;
+    qf.vol = p->vol;
+    qf.mirror = p->mirror;
+    qf.rou = p->d_rou;
+    qf.perm = p->d_perm;
+    qf.betaw = p->d_betaw;
+    p->tp_fft<<<dim3(p->tp_ntiles, ch.count), p->tp_threads, p->tp_fft_smem, s>>>(qf);
+    p->launches += 1;
   } else {
     dim3 grid(p->n_col_tiles, (ch.count + MT - 1) / MT);
+    if (prm.group_major) grid = dim3((ch.count + MT - 1) / MT, p->n_col_tiles);
     couple_kernel(p->n, p->MG, p->NG)<<<grid, couple_threads(p->n), p->couple_smem, s>>>(prm);
   }
   CKL();

@@ -1,15 +1,16 @@
 """Summarise an ncu report of k_couple: SOL numbers, stall reasons, and SASS samples per
-barrier-delimited phase. Usage: python tools/ncu_phases.py report.ncu-rep"""
+barrier-delimited phase. Usage: python tools/ncu_phases.py report.ncu-rep [kernel-name regex]"""
 import csv
 import io
 import subprocess
 import sys
 
 rep = sys.argv[1]
+kfilter = ["--kernel-name", "regex:" + sys.argv[2]] if len(sys.argv) > 2 else []
 
 
 def ncu(*args):
-    return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
+    return subprocess.run(["ncu", "-i", rep, *kfilter, *args], capture_output=True, text=True).stdout
 
 
 raw = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
@@ -35,7 +36,7 @@ tot = sum(v for v, _ in items) or 1
 print("stalls:", ", ".join(f"{k.split('stalled_')[1]} {100*v/tot:.1f}%" for v, k in sorted(items, reverse=True)[:8]))
 rows = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-source", "sass"))))
 h = rows[1]
-data = rows[2:]
+data = [r for r in rows[2:] if r != h and len(r) == len(h)]
 iS, iW, iE = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
 tot = sum(float(r[iW] or 0) for r in data) or 1
 acc = ex = 0.0
