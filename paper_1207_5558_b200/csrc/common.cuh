@@ -17,6 +17,14 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// Same MMA as a non-volatile asm: the compiler may schedule fragment loads and other MMAs
+// around it (the result is only consumed through its outputs).
+__device__ __forceinline__ void dmma_nv(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
 struct CompRec {
   int l, m;
   long long slot;   // output volume slot of (l, m)

@@ -16,6 +16,8 @@
 // sample, but lets the GEMM run on 64x64 tiles (8x the operand reuse).
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels_chunk.cuh"
 #include "kernels_couple.cuh"
@@ -23,12 +25,11 @@
 namespace slsht_cuda {
 
 constexpr int TG_BM = 64;      // components per CTA
-constexpr int TG_BN = 64;      // grid columns per CTA
+constexpr int TG_BN = 64;      // column padding unit of W and T (the widest CTA tile)
 constexpr int TG_KS = 16;      // (p, q) rows per pipeline stage (4 k-steps)
 constexpr int TG_NST = 4;      // pipeline depth
 constexpr int TG_ASTR = 20;    // A row stride (complex): == 4 mod 8, conflict-free fragments
-constexpr int TG_BSTR = 66;    // B row stride (complex): == 2 mod 8, conflict-free fragments
-constexpr int TG_THREADS = 256;
+// B row stride (complex) BN + 2 == 2 mod 8: conflict-free fragments
 
 struct TgParams {
   const double2* U;      // [comp][KP]: q-major padded (p, q) rows, zero padding
@@ -38,8 +39,9 @@ struct TgParams {
   int count, KP, ncolp, n;
 };
 
-__host__ __device__ constexpr size_t tgemm_smem_bytes(int KP) {
-  return (size_t)TG_NST * (TG_BM * TG_ASTR + TG_KS * TG_BSTR) * 16 + (size_t)(KP / 4) * 2 + 16;
+__host__ __device__ constexpr int tgemm_threads(int BN) { return 64 * (BN / 16); }
+__host__ __device__ constexpr size_t tgemm_smem_bytes(int KP, int BN) {
+  return (size_t)TG_NST * (TG_BM * TG_ASTR + TG_KS * (BN + 2)) * 16 + (size_t)(KP / 4) * 2 + 16;
 }
 
 // 256-bit global store (sm_100): two consecutive complex values
@@ -48,7 +50,11 @@ __device__ __forceinline__ void st_global_v4(double2* p, double a, double b, dou
                : "memory");
 }
 
-__global__ void __launch_bounds__(TG_THREADS, 1) k_tgemm(const TgParams P) {
+// BN = 64: 8 warps, one CTA per SM. BN = 32: 4 warps (117 KB), which leaves room on the SM
+// for one k_qfft CTA of the previous chunk (the overlapped schedule).
+template <int BN>
+__global__ void __launch_bounds__(tgemm_threads(BN), 1) k_tgemm(const TgParams P) {
+  constexpr int TG_THREADS = tgemm_threads(BN), TG_BSTR = BN + 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As = reinterpret_cast<double2*>(smem_raw);
   double2* Bs = As + TG_NST * TG_BM * TG_ASTR;
@@ -56,7 +62,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1) k_tgemm(const TgParams P) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // grid x = component block: the CTAs in flight share a few W column tiles (read from HBM
   // once per chunk) while the chunk's U stays L2-resident
-  const int comp0 = blockIdx.x * TG_BM, col0 = blockIdx.y * TG_BN;
+  const int comp0 = blockIdx.x * TG_BM, col0 = blockIdx.y * BN;
   const int nks = P.KP / 4, nst = (P.KP + TG_KS - 1) / TG_KS;
   for (int i = tid; i < nks; i += TG_THREADS) qend_s[i] = P.qend[i];
 
@@ -73,9 +79,9 @@ __global__ void __launch_bounds__(TG_THREADS, 1) k_tgemm(const TgParams P) {
         cp_async16(Ad + c * TG_ASTR + k, P.U + (ok ? (size_t)(comp0 + c) * P.KP + kb + k : 0), ok);
       }
 #pragma unroll
-      for (int j = 0; j < TG_KS * TG_BN / TG_THREADS; ++j) {
+      for (int j = 0; j < TG_KS * BN / TG_THREADS; ++j) {
         const int e = tid + j * TG_THREADS;
-        const int k = e / TG_BN, c = e % TG_BN;
+        const int k = e / BN, c = e % BN;
         const bool ok = kb + k < P.KP;
         cp_async16(Bd + k * TG_BSTR + c, P.W + (ok ? (size_t)(kb + k) * P.ncolp + col0 + c : 0), ok);
       }
@@ -86,7 +92,8 @@ __global__ void __launch_bounds__(TG_THREADS, 1) k_tgemm(const TgParams P) {
   for (int s = 0; s < TG_NST - 1; ++s) load_stage(s);
 
   // warp tile: 32 components (4 MMA rows) x 16 columns (2 MMA columns)
-  const int wm = warp >> 2, wn = warp & 3;
+  constexpr int WN = BN / 16;
+  const int wm = warp / WN, wn = warp % WN;
   const int arow = wm * 32 + (lane >> 2), acol = lane & 3;
   const int brow = lane & 3, bcol = wn * 16 + (lane >> 2);
   double c1[4][2][2], c2[4][2][2], c3[4][2][2];
@@ -123,9 +130,9 @@ __global__ void __launch_bounds__(TG_THREADS, 1) k_tgemm(const TgParams P) {
         const double bd = b[ni].y - b[ni].x, bs = b[ni].x + b[ni].y;
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
-          dmma(c1[mi][ni][0], c1[mi][ni][1], a[mi].x + a[mi].y, b[ni].x);
-          dmma(c2[mi][ni][0], c2[mi][ni][1], a[mi].x, bd);
-          dmma(c3[mi][ni][0], c3[mi][ni][1], a[mi].y, bs);
+          dmma_nv(c1[mi][ni][0], c1[mi][ni][1], a[mi].x + a[mi].y, b[ni].x);
+          dmma_nv(c2[mi][ni][0], c2[mi][ni][1], a[mi].x, bd);
+          dmma_nv(c3[mi][ni][0], c3[mi][ni][1], a[mi].y, bs);
         }
       }
       const int row = qend_s[ks];
@@ -180,6 +187,11 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
   double* betaw_s = reinterpret_cast<double*>(rou_s + N);
   int* perm_s = reinterpret_cast<int*>(betaw_s + (L + 1));
   const int tid = threadIdx.x;
+  for (int i = tid; i < N; i += NTHR) {
+    rou_s[i] = P.rou[i];
+    perm_s[i] = P.perm[i];
+  }
+  for (int i = tid; i <= L; i += NTHR) betaw_s[i] = P.betaw[i];
   const int ct = blockIdx.x, comp = blockIdx.y;
   const int col0 = ct * NT;
   {
@@ -190,11 +202,6 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
     }
     cp_async_commit();
   }
-  for (int i = tid; i < N; i += NTHR) {
-    rou_s[i] = P.rou[i];
-    perm_s[i] = P.perm[i];
-  }
-  for (int i = tid; i <= L; i += NTHR) betaw_s[i] = P.betaw[i];
   cp_async_wait<0>();
   __syncthreads();
 
@@ -223,25 +230,31 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
       g0r = t.x;
       g0i = t.y;
     }
-    for (int a = a_first; a < N; a += A_STEP, hsh += hstep) {
-      const double2 t = Tp[(size_t)perm_s[a] * NT];
-      const double vr = t.x, vi = t.y;
-      const size_t idx = (size_t)a * P.ncol;
-      __stcs(o + idx, make_double2(vr, vi));
-      if (om) {
-        const long long br = __double_as_longlong(vr) ^ mflip_r;
-        const long long bi = __double_as_longlong(vi) ^ mflip_i;
-        __stcs(om + idx, make_double2(__longlong_as_double(br), __longlong_as_double(bi)));
+    auto rows = [&](auto mirror_tag) {
+      constexpr bool MIR = decltype(mirror_tag)::value;
+#pragma unroll 4
+      for (int a = a_first; a < N; a += A_STEP, hsh += hstep) {
+        const double2 t = Tp[(size_t)perm_s[a] * NT];
+        const double vr = t.x, vi = t.y;
+        const size_t idx = (size_t)a * P.ncol;
+        __stcs(o + idx, make_double2(vr, vi));
+        if constexpr (MIR) {
+          const long long br = __double_as_longlong(vr) ^ mflip_r;
+          const long long bi = __double_as_longlong(vi) ^ mflip_i;
+          __stcs(om + idx, make_double2(__longlong_as_double(br), __longlong_as_double(bi)));
+        }
+        const double a2 = fma(vr, vr, vi * vi);
+        s2 += a2;
+        mx2 = max(mx2, __double_as_longlong(a2));
+        const double wgt = digest_weight(hsh);
+        pr = fma(wgt, vr, pr);
+        pi = fma(wgt, vi, pi);
+        ir += vr;
+        ii += vi;
       }
-      const double a2 = fma(vr, vr, vi * vi);
-      s2 += a2;
-      mx2 = max(mx2, __double_as_longlong(a2));
-      const double wgt = digest_weight(hsh);
-      pr = fma(wgt, vr, pr);
-      pi = fma(wgt, vi, pi);
-      ir += vr;
-      ii += vi;
-    }
+    };
+    if (om) rows(std::true_type{});
+    else rows(std::false_type{});
     ir *= qb;
     ii *= qb;
   }

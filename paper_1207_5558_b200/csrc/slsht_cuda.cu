@@ -118,6 +118,13 @@ struct slsht_cuda_plan {
   int tp_ntiles = 0;       //   k_qfft column tiles (digest partials per component)
   int tp_threads = 0;
   size_t tp_gemm_smem = 0, tp_fft_smem = 0;
+  int tp_bn = 64;          //   k_tgemm column tile (32 in the overlapped schedule)
+  bool tp_overlap = false; //   k_qfft + digest of chunk i on fft_stream under k_tgemm of i+1
+  size_t tp_t_elems = 0;   //   one T buffer (two in the overlapped schedule)
+  cudaStream_t fft_stream = nullptr;
+  cudaEvent_t ev_tg[2] = {}, ev_fft[2] = {};
+  bool fft_rec[2] = {false, false};  // ev_fft[b] recorded during the current call
+  int fft_last = -1;
   void (*tp_fft)(QfParams) = nullptr;
   int* d_ubase = nullptr;  // stage-tiled U layout (ws path): per (p, q) row block offset
   int* d_ustr = nullptr;   //   and row stride
@@ -220,6 +227,11 @@ void free_plan(slsht_cuda_plan* p) {
   for (auto& e : p->ev_lazy)
     if (e) cudaEventDestroy(e);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->fft_stream) cudaStreamDestroy(p->fft_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (p->ev_tg[i]) cudaEventDestroy(p->ev_tg[i]);
+    if (p->ev_fft[i]) cudaEventDestroy(p->ev_fft[i]);
+  }
   if (p->aux_stream) {
     cudaStreamSynchronize(p->aux_stream);
     cudaStreamDestroy(p->aux_stream);
@@ -668,7 +680,14 @@ void build_plan(slsht_cuda_plan* p) {
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   const size_t out_bytes = (size_t)p->n_slots * vol_bytes;
-  const size_t t_bytes = p->use_tp ? (size_t)p->max_chunk * p->n * p->tp_ncolp * 16 : 0;
+  // overlapped schedule (multi-chunk plans, SLSHT_CUDA_TP_OVERLAP=1): two T buffers
+  if (p->use_tp) {
+    const char* e = std::getenv("SLSHT_CUDA_TP_OVERLAP");
+    p->tp_overlap = p->chunks.size() > 1 && e && e[0] == '1';  // measured slower: opt-in
+    p->tp_bn = p->tp_overlap ? 32 : 64;
+    p->tp_t_elems = (size_t)p->max_chunk * p->n * p->tp_ncolp;
+  }
+  const size_t t_bytes = p->use_tp ? p->tp_t_elems * 16 * (p->tp_overlap ? 2 : 1) : 0;
   if (out_bytes + t_bytes + (64u << 20) > free_b)
     throw Status{SLSHT_ERR_VALIDATION,
                  "device output buffer does not fit in HBM (use the streaming ring mode)"};
@@ -697,11 +716,18 @@ void build_plan(slsht_cuda_plan* p) {
     CK(cudaFuncSetAttribute(p->lines_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)p->couple_smem));
   } else if (p->use_tp) {
-    p->tp_gemm_smem = tgemm_smem_bytes(p->tp_KP);
+    p->tp_gemm_smem = tgemm_smem_bytes(p->tp_KP, p->tp_bn);
     p->tp_fft_smem = qfft_smem_bytes(p->n);
     p->couple_smem = std::max(p->tp_gemm_smem, p->tp_fft_smem);
-    CK(cudaFuncSetAttribute(k_tgemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)p->tp_gemm_smem));
+    CK(cudaFuncSetAttribute(p->tp_bn == 32 ? k_tgemm<32> : k_tgemm<64>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tp_gemm_smem));
+    if (p->tp_overlap) {
+      CK(cudaStreamCreateWithFlags(&p->fft_stream, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&p->ev_tg[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&p->ev_fft[i], cudaEventDisableTiming));
+      }
+    }
     CK(cudaFuncSetAttribute(p->tp_fft, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)p->tp_fft_smem));
   } else if (p->use_ws) {
@@ -774,6 +800,13 @@ void join_aux(slsht_cuda_plan* p) {
 // Two independent chains: nodes -> Legendre window rows -> I table (needed by the modulated
 // SHT) on the main stream, and Delta -> d tables -> window table W (needed only by the
 // coupling) on the auxiliary stream, where it overlaps the node chain and the modulated SHT.
+// The main stream waits for the last k_qfft/digest of the overlapped schedule.
+void join_fft(slsht_cuda_plan* p) {
+  if (p->fft_last < 0) return;
+  CK(cudaStreamWaitEvent(p->stream, p->ev_fft[p->fft_last], 0));
+  p->fft_last = -1;
+}
+
 void run_setup(slsht_cuda_plan* p) {
   cudaStream_t s = p->stream;
   const int L = p->L_h;
@@ -824,6 +857,7 @@ void run_setup(slsht_cuda_plan* p) {
 
 void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   cudaStream_t s = p->stream;
+  if (&ch == &p->chunks.front()) p->fft_rec[0] = p->fft_rec[1] = false;  // a new call
   const CompRec* comps = p->d_comps + ch.comp0;
   record(p, 0);
   k_agen<<<dim3(ch.nseg, (p->ldA + 127) / 128), 128, 3 * (p->L_g + 1) * sizeof(double), s>>>(
@@ -930,20 +964,48 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     }
 #endif
   } else if (p->use_tp) {
+    // overlapped schedule: T buffer b = chunk parity; k_tgemm waits until the k_qfft that read
+    // T[b] two chunks ago is done, and k_qfft + digest run on fft_stream
+    const bool overlap = p->tp_overlap && !p->profile;
+    const int b = overlap ? ch.buf : 0;
+    if (overlap && p->fft_rec[b]) CK(cudaStreamWaitEvent(s, p->ev_fft[b], 0));
     TgParams tg{};
     tg.U = p->d_U;
     tg.W = p->d_W;
-    tg.T = p->d_T;
+    tg.T = p->d_T + b * p->tp_t_elems;
     tg.qend = p->d_qend;
     tg.count = ch.count;
     tg.KP = p->tp_KP;
     tg.ncolp = p->tp_ncolp;
     tg.n = p->n;
-    k_tgemm<<<dim3((ch.count + TG_BM - 1) / TG_BM, p->tp_ncolp / TG_BN), TG_THREADS,
-              p->tp_gemm_smem, s>>>(tg);
+    const dim3 tgrid((ch.count + TG_BM - 1) / TG_BM, p->tp_ncolp / p->tp_bn);
+    if (p->tp_bn == 32) {
+      // the GEMM of chunk i+1 is dispatched ahead of the FFT CTAs of chunk i (one GEMM CTA per
+      // SM, one FFT CTA beside it)
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = tgrid;
+      lc.blockDim = dim3(tgemm_threads(32));
+      lc.dynamicSmemBytes = p->tp_gemm_smem;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributePriority;
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      at[0].val.priority = hi;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&lc, k_tgemm<32>, tg));
+    } else
+      k_tgemm<64><<<tgrid, tgemm_threads(64), p->tp_gemm_smem, s>>>(tg);
     CKL();
+    cudaStream_t fs = s;
+    if (overlap) {
+      CK(cudaEventRecord(p->ev_tg[b], s));
+      CK(cudaStreamWaitEvent(p->fft_stream, p->ev_tg[b], 0));
+      fs = p->fft_stream;
+    }
     QfParams qf{};
-    qf.T = p->d_T;
+    qf.T = tg.T;
     qf.out = p->d_out;
     qf.partials = p->d_partials;
     qf.comps = comps;
@@ -957,7 +1019,18 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     qf.rou = p->d_rou;
     qf.perm = p->d_perm;
     qf.betaw = p->d_betaw;
-    p->tp_fft<<<dim3(p->tp_ntiles, ch.count), p->tp_threads, p->tp_fft_smem, s>>>(qf);
+    p->tp_fft<<<dim3(p->tp_ntiles, ch.count), p->tp_threads, p->tp_fft_smem, fs>>>(qf);
+    CKL();
+    if (overlap) {
+      k_digest<<<(ch.count + 3) / 4, 128, 0, fs>>>(comps, ch.count, p->n_col_tiles, p->n,
+                                                    p->d_partials, p->mirror, p->d_digest);
+      CKL();
+      CK(cudaEventRecord(p->ev_fft[b], fs));
+      p->fft_rec[b] = true;
+      p->fft_last = b;
+      p->launches += 3;
+      return;
+    }
     p->launches += 1;
   } else {
     dim3 grid(p->n_col_tiles, (ch.count + MT - 1) / MT);
@@ -1087,6 +1160,7 @@ void run_forward_device(slsht_cuda_plan* p, const double* f, const double* h,
       try {
         run_setup(p);
         for (const Chunk& ch : p->chunks) run_chunk(p, ch);
+        join_fft(p);
         join_aux(p);
       } catch (...) {
         cudaStreamEndCapture(p->stream, &graph);
@@ -1107,6 +1181,7 @@ void run_forward_device(slsht_cuda_plan* p, const double* f, const double* h,
     } else {
       run_setup(p);
       for (const Chunk& ch : p->chunks) run_chunk(p, ch);
+      join_fft(p);
       join_aux(p);
     }
     if (digests) copy_digests(p, digests, digests_on_device != 0);
@@ -1162,6 +1237,7 @@ int slsht_cuda_forward_capture(slsht_cuda_plan* p, const double* f, const double
     run_setup(p);
     for (size_t ci = 0; ci < p->chunks.size(); ++ci) {
       run_chunk(p, p->chunks[ci]);
+      join_fft(p);
       for (const Req& r : reqs)
         if (r.chunk == ci)
           CK(cudaMemcpyAsync(volumes + 2 * (size_t)r.i * p->vol, p->d_out + (size_t)r.slot * p->vol,
@@ -1214,6 +1290,7 @@ int slsht_cuda_forward(slsht_cuda_plan* p, const double* f, const double* h, sls
       run_chunk(p, ch);
       CK(cudaEventRecord(p->ev_done[ch.buf], p->stream));
       CK(cudaStreamWaitEvent(p->copy_stream, p->ev_done[ch.buf], 0));
+      if (p->fft_last >= 0) CK(cudaStreamWaitEvent(p->copy_stream, p->ev_fft[ch.buf], 0));
       const double2* src = p->d_out + (size_t)ch.buf * per * p->max_chunk * p->vol;
       CK(cudaMemcpyAsync(p->h_stage[ch.buf], src, (size_t)ch.count * vb, cudaMemcpyDeviceToHost,
                          p->copy_stream));
@@ -1226,6 +1303,7 @@ int slsht_cuda_forward(slsht_cuda_plan* p, const double* f, const double* h, sls
     const size_t nc = p->chunks.size();
     if (nc >= 2) deliver(nc - 2);
     if (nc >= 1) deliver(nc - 1);
+    join_fft(p);
     CK(cudaStreamSynchronize(p->stream));
   });
 }
