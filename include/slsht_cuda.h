@@ -109,7 +109,8 @@ void* slsht_cuda_stream(const slsht_cuda_plan* plan);
  * events on the plan stream) when profiling is on (slsht_cuda_set_profiling, or
  * SLSHT_CUDA_PROFILE=1 at plan creation):
  * out[0] setup tables, [1] Legendre rows, [2] modulated-SHT GEMM, [3] coupling + alpha FFT
- * + epilogue, [4] digest reduction. Returns the number of entries written. */
+ * + epilogue (two-pass path: the k_tgemm GEMM only), [4] digest reduction, [5] two-pass path:
+ * k_qfft (alpha FFT + epilogue), 0 on the other paths. Returns the number of entries written. */
 long long slsht_cuda_launch_count(const slsht_cuda_plan* plan);
 int slsht_cuda_stage_times(const slsht_cuda_plan* plan, double* out_ms, int n);
 /* Turn per-stage event timing on or off for subsequent forward calls (adds one host

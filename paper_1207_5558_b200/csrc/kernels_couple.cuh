@@ -47,8 +47,9 @@ constexpr int smallest_prime_factor(int n) {
 }
 
 // One DIF stage of radix R on sub-transforms of span S (compile-time N), executed by the
-// NTHR threads numbered tid = 0..NTHR-1.
-template <int N, int R, int S, int NT, int PAIRS, int NTHR>
+// NTHR threads numbered tid = 0..NTHR-1. SINK: the twiddle-free last stage of a radix with a
+// streaming butterfly (Radix<R>::dft_sink) stores each output as soon as it is formed.
+template <int N, int R, int S, int NT, int PAIRS, int NTHR, bool SINK = false>
 __device__ __forceinline__ void fft_stage_ct(double2* T, const double2* rou_s, int tid) {
   constexpr int MP = S / R;
   constexpr int TOTAL = PAIRS * (N / R);
@@ -64,6 +65,12 @@ __device__ __forceinline__ void fft_stage_ct(double2* T, const double2* rou_s, i
       const double2 v = base[k * MP * NT];
       xr[k] = v.x;
       xi[k] = v.y;
+    }
+    if constexpr (SINK && MP == 1 && R >= kSinkMinRadix) {
+      Radix<R>::dft_sink(xr, xi, [&](int k, double yr, double yi) {
+        base[k * NT] = make_double2(yr, yi);
+      });
+      continue;
     }
     Radix<R>::dft(xr, xi);
     base[0] = make_double2(xr[0], xi[0]);
@@ -87,18 +94,18 @@ __device__ __forceinline__ void stage_sync(int bar, int count) {
 
 // Full DIF plan: radices = prime factors of N in ascending order (the host's perm matches).
 // bar 0 synchronizes the whole CTA, bar > 0 only the NTHR participating threads.
-template <int N, int S, int NT, int PAIRS, int NTHR>
+template <int N, int S, int NT, int PAIRS, int NTHR, bool SINK = false>
 struct FftDif {
   __device__ __forceinline__ static void run(double2* T, const double2* rou_s, int tid, int bar) {
     constexpr int R = smallest_prime_factor(S);
     static_assert(Radix<R>::kSupported, "no generated butterfly for this radix");
-    fft_stage_ct<N, R, S, NT, PAIRS, NTHR>(T, rou_s, tid);
+    fft_stage_ct<N, R, S, NT, PAIRS, NTHR, SINK>(T, rou_s, tid);
     stage_sync(bar, NTHR);
-    FftDif<N, S / R, NT, PAIRS, NTHR>::run(T, rou_s, tid, bar);
+    FftDif<N, S / R, NT, PAIRS, NTHR, SINK>::run(T, rou_s, tid, bar);
   }
 };
-template <int N, int NT, int PAIRS, int NTHR>
-struct FftDif<N, 1, NT, PAIRS, NTHR> {
+template <int N, int NT, int PAIRS, int NTHR, bool SINK>
+struct FftDif<N, 1, NT, PAIRS, NTHR, SINK> {
   __device__ __forceinline__ static void run(double2*, const double2*, int, int) {}
 };
 

@@ -27,12 +27,11 @@ namespace slsht_cuda {
 constexpr int TG_BM = 64;      // components per CTA
 constexpr int TG_BN = 64;      // column padding unit of W and T (the widest CTA tile)
 constexpr int TG_KS = 16;      // (p, q) rows per pipeline stage (4 k-steps)
-constexpr int TG_NST = 4;      // pipeline depth
 constexpr int TG_ASTR = 20;    // A row stride (complex): == 4 mod 8, conflict-free fragments
 // B row stride (complex) BN + 2 == 2 mod 8: conflict-free fragments
 
 struct TgParams {
-  const double2* U;      // [comp][KP]: q-major padded (p, q) rows, zero padding
+  const double2* U;      // [comp][KP]: q-major padded (p, q) rows, zero padding; KP % TG_KS == 0
   const double2* W;      // [KP][ncolp]
   double2* T;            // [comp][n][ncolp]
   const short* qend;     // per k-step: T row (q mod n) completed by it, or -1
@@ -40,8 +39,8 @@ struct TgParams {
 };
 
 __host__ __device__ constexpr int tgemm_threads(int BN) { return 64 * (BN / 16); }
-__host__ __device__ constexpr size_t tgemm_smem_bytes(int KP, int BN) {
-  return (size_t)TG_NST * (TG_BM * TG_ASTR + TG_KS * (BN + 2)) * 16 + (size_t)(KP / 4) * 2 + 16;
+__host__ __device__ constexpr size_t tgemm_smem_bytes(int KP, int BN, int NST) {
+  return (size_t)NST * (TG_BM * TG_ASTR + TG_KS * (BN + 2)) * 16 + (size_t)(KP / 4) * 2 + 16;
 }
 
 // 256-bit global store (sm_100): two consecutive complex values
@@ -50,10 +49,11 @@ __device__ __forceinline__ void st_global_v4(double2* p, double a, double b, dou
                : "memory");
 }
 
-// BN = 64: 8 warps, one CTA per SM. BN = 32: 4 warps (117 KB), which leaves room on the SM
-// for one k_qfft CTA of the previous chunk (the overlapped schedule).
-template <int BN>
-__global__ void __launch_bounds__(tgemm_threads(BN), 1) k_tgemm(const TgParams P) {
+// <64, 4, 1>: 8 warps, one CTA per SM. <32, 3, 2>: 4 warps, two independent CTAs per SM.
+// <32, 4, 1>: 4 warps (117 KB), which leaves room on the SM for one k_qfft CTA of the previous
+// chunk (the overlapped schedule).
+template <int BN, int TG_NST, int MINB>
+__global__ void __launch_bounds__(tgemm_threads(BN), MINB) k_tgemm(const TgParams P) {
   constexpr int TG_THREADS = tgemm_threads(BN), TG_BSTR = BN + 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As = reinterpret_cast<double2*>(smem_raw);
@@ -117,24 +117,33 @@ __global__ void __launch_bounds__(tgemm_threads(BN), 1) k_tgemm(const TgParams P
     const double2* Bb = Bs + (st % TG_NST) * TG_KS * TG_BSTR;
 #pragma unroll
     for (int kk = 0; kk < TG_KS / 4; ++kk) {
-      const int ks = st * (TG_KS / 4) + kk;
-      if (ks >= nks) break;
+      const int ks = st * (TG_KS / 4) + kk;  // KP is a multiple of TG_KS: no partial stage
       double2 a[4], b[2];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) a[mi] = Ab[(arow + mi * 8) * TG_ASTR + kk * 4 + acol];
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni) b[ni] = Bb[(kk * 4 + brow) * TG_BSTR + bcol + ni * 8];
       // Gauss: K1 += (ar+ai) br, K2 += ar (bi-br), K3 += ai (br+bi); re = K1-K3, im = K1+K2
+      double as[4], bd[2], bs[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) as[mi] = a[mi].x + a[mi].y;
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni) {
-        const double bd = b[ni].y - b[ni].x, bs = b[ni].x + b[ni].y;
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi) {
-          dmma_nv(c1[mi][ni][0], c1[mi][ni][1], a[mi].x + a[mi].y, b[ni].x);
-          dmma_nv(c2[mi][ni][0], c2[mi][ni][1], a[mi].x, bd);
-          dmma_nv(c3[mi][ni][0], c3[mi][ni][1], a[mi].y, bs);
-        }
+        bd[ni] = b[ni].y - b[ni].x;
+        bs[ni] = b[ni].x + b[ni].y;
       }
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) dmma(c1[mi][ni][0], c1[mi][ni][1], as[mi], b[ni].x);
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) dmma(c2[mi][ni][0], c2[mi][ni][1], a[mi].x, bd[ni]);
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) dmma(c3[mi][ni][0], c3[mi][ni][1], a[mi].y, bs[ni]);
       const int row = qend_s[ks];
       if (row >= 0) {
 #pragma unroll
@@ -148,16 +157,26 @@ __global__ void __launch_bounds__(tgemm_threads(BN), 1) k_tgemm(const TgParams P
                            c1[mi][ni][1] - c3[mi][ni][1], c1[mi][ni][1] + c2[mi][ni][1]);
           }
         }
-        reset();
       }
+      // branch-free reset (a conditional reset inside the branch makes the compiler route
+      // every MMA result through register copies)
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            c1[mi][ni][e] = row >= 0 ? 0.0 : c1[mi][ni][e];
+            c2[mi][ni][e] = row >= 0 ? 0.0 : c2[mi][ni][e];
+            c3[mi][ni][e] = row >= 0 ? 0.0 : c3[mi][ni][e];
+          }
     }
   }
   cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------------------------
-// k_qfft: one component x QF_NT grid columns per CTA.
-constexpr int QF_NT = 32;
+// k_qfft: one component x NT grid columns per CTA.
 
 struct QfParams {
   const double2* T;      // [comp][n][ncolp]
@@ -172,13 +191,12 @@ struct QfParams {
   const double* betaw;
 };
 
-__host__ __device__ constexpr size_t qfft_smem_bytes(int n) {
-  return (size_t)n * QF_NT * 16 + (size_t)n * 16 + (size_t)((n + 1) / 2) * 8 + (size_t)n * 4 + 64;
+__host__ __device__ constexpr size_t qfft_smem_bytes(int n, int NT) {
+  return (size_t)n * NT * 16 + (size_t)n * 16 + (size_t)((n + 1) / 2) * 8 + (size_t)n * 4 + 64;
 }
 
-template <int N, int NTHR, int MINB>
+template <int N, int NT, int NTHR, int MINB>
 __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
-  constexpr int NT = QF_NT;
   constexpr int L = (N - 1) / 2;
   static_assert(NTHR % NT == 0, "threads must cover whole column sets");
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -205,7 +223,7 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
   cp_async_wait<0>();
   __syncthreads();
 
-  FftDif<N, N, NT, NT, NTHR>::run(Ts, rou_s, tid, 0);
+  FftDif<N, N, NT, NT, NTHR, true>::run(Ts, rou_s, tid, 0);
 
   // epilogue: thread = (column cc, first row a_first); stores row by row (a warp writes 32
   // consecutive samples of one row), the mirror volume with sign flips, digest partials

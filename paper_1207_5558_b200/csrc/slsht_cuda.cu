@@ -74,7 +74,8 @@ struct Chunk {
   int buf;  // ring half (ring mode)
 };
 
-enum Stage { ST_SETUP = 0, ST_LEGENDRE, ST_MODGEMM, ST_COUPLE, ST_DIGEST, ST_COUNT };
+// ST_QFFT: the two-pass path's k_qfft (its k_tgemm is ST_COUPLE); 0 on the other paths
+enum Stage { ST_SETUP = 0, ST_LEGENDRE, ST_MODGEMM, ST_COUPLE, ST_DIGEST, ST_QFFT, ST_COUNT };
 
 // Warp-specialized persistent kernels (kernels_couple_ws.cuh) for the BASELINE lengths.
 struct WsKernel {
@@ -116,9 +117,11 @@ struct slsht_cuda_plan {
   int tp_KP = 0;           //   q-padded (p, q) rows
   int tp_ncolp = 0;        //   padded column stride of W and T
   int tp_ntiles = 0;       //   k_qfft column tiles (digest partials per component)
+  int tp_nt = 32;          //   k_qfft columns per CTA
   int tp_threads = 0;
   size_t tp_gemm_smem = 0, tp_fft_smem = 0;
   int tp_bn = 64;          //   k_tgemm column tile (32 in the overlapped schedule)
+  int tp_gv = 1;           //   k_tgemm variant: 0 <64,4,1>, 1 <32,3,2>, 2 <32,4,1>
   bool tp_overlap = false; //   k_qfft + digest of chunk i on fft_stream under k_tgemm of i+1
   size_t tp_t_elems = 0;   //   one T buffer (two in the overlapped schedule)
   cudaStream_t fft_stream = nullptr;
@@ -139,7 +142,7 @@ struct slsht_cuda_plan {
   bool profile = false;
   std::string last_error;
   long long launches = 0;
-  double stage_ms[ST_COUNT] = {0, 0, 0, 0, 0};
+  double stage_ms[ST_COUNT] = {0, 0, 0, 0, 0, 0};
 
   std::vector<CompRec> comps;
   std::vector<Seg> segs;
@@ -305,14 +308,34 @@ bool ws_kernel(int n, WsKernel& k) {
   }
 }
 
+using TgemmFn = void (*)(TgParams);
+TgemmFn tgemm_kernel(int v) {
+  return v == 1 ? k_tgemm<32, 3, 2> : (v == 2 ? k_tgemm<32, 4, 1> : k_tgemm<64, 4, 1>);
+}
+
 // Two-pass coupling (kernels_twopass.cuh): the k_qfft instantiation per BASELINE length.
-bool tp_kernel(int n, void (*&fn)(QfParams), int& threads) {
+// SLSHT_CUDA_QFFT=1 / 2 select the experimental shapes (96 threads; 16 columns x 64 threads).
+bool tp_kernel(int n, void (*&fn)(QfParams), int& threads, int& nt) {
+  const char* e = std::getenv("SLSHT_CUDA_QFFT");
+  const int v = e ? std::atoi(e) : 0;
+  threads = 128;
+  nt = 32;
   switch (n) {
-    case 65: fn = k_qfft<65, 128, 4>; break;
-    case 129: fn = k_qfft<129, 128, 2>; break;
+    case 65: fn = k_qfft<65, 32, 128, 4>; break;
+    case 129:
+      if (v == 1) {
+        fn = k_qfft<129, 32, 96, 2>;
+        threads = 96;
+      } else if (v == 2) {
+        fn = k_qfft<129, 16, 64, 4>;
+        threads = 64;
+        nt = 16;
+      } else {
+        fn = k_qfft<129, 32, 128, 2>;
+      }
+      break;
     default: return false;
   }
-  threads = 128;
   return true;
 }
 
@@ -356,9 +379,15 @@ void build_plan(slsht_cuda_plan* p) {
   // k_couple then runs); n = 33 keeps its line kernel, n = 17 its warp-specialized kernel
   {
     const char* e = std::getenv("SLSHT_CUDA_TWO_PASS");
-    p->use_tp = !(e && e[0] == '0') && tp_kernel(p->n, p->tp_fft, p->tp_threads);
+    p->use_tp = !(e && e[0] == '0') && tp_kernel(p->n, p->tp_fft, p->tp_threads, p->tp_nt);
     p->tp_ncolp = (p->ncol + TG_BN - 1) / TG_BN * TG_BN;
-    p->tp_ntiles = (p->ncol + QF_NT - 1) / QF_NT;
+    p->tp_ntiles = (p->ncol + p->tp_nt - 1) / p->tp_nt;
+    // k_tgemm shape: <32, 3, 2> (two 4-warp CTAs per SM) unless SLSHT_CUDA_TGEMM selects
+    // <64, 4, 1> (0) or <32, 4, 1> (2)
+    const char* gv = std::getenv("SLSHT_CUDA_TGEMM");
+    p->tp_gv = gv ? std::atoi(gv) : 1;
+    if (p->tp_gv < 0 || p->tp_gv > 2) p->tp_gv = 1;
+    p->tp_bn = p->tp_gv == 0 ? 64 : 32;
   }
   // ---- component list: orders m (all or m >= 0 in real mode), degrees in the shard
   for (int m = p->real_mode ? 0 : -p->lmax; m <= p->lmax; ++m) {
@@ -392,7 +421,8 @@ void build_plan(slsht_cuda_plan* p) {
       int sms = 148;
       if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device) != cudaSuccess)
         sms = 148;
-      const long long nct = p->tp_ncolp / TG_BN, bmax = ch / TG_BM;
+      sms *= p->tp_gv == 1 ? 2 : 1;  // resident k_tgemm CTAs
+      const long long nct = p->tp_ncolp / p->tp_bn, bmax = ch / TG_BM;
       long long best_b = bmax;
       double best = 0.0;
       for (long long b = bmax; b >= (bmax + 1) / 2; --b) {
@@ -536,6 +566,7 @@ void build_plan(slsht_cuda_plan* p) {
       rows_pad += (qoff[jq + 1] - qoff[jq] + 3) / 4 * 4;
     }
     urb[p->n] = rows_pad;
+    rows_pad = (rows_pad + TG_KS - 1) / TG_KS * TG_KS;  // whole GEMM stages (zero rows)
     p->tp_KP = rows_pad;
     qend.assign(rows_pad / 4, (short)-1);
     for (int jq = 0; jq < p->n; ++jq) {
@@ -684,7 +715,10 @@ void build_plan(slsht_cuda_plan* p) {
   if (p->use_tp) {
     const char* e = std::getenv("SLSHT_CUDA_TP_OVERLAP");
     p->tp_overlap = p->chunks.size() > 1 && e && e[0] == '1';  // measured slower: opt-in
-    p->tp_bn = p->tp_overlap ? 32 : 64;
+    if (p->tp_overlap) {
+      p->tp_gv = 2;
+      p->tp_bn = 32;
+    }
     p->tp_t_elems = (size_t)p->max_chunk * p->n * p->tp_ncolp;
   }
   const size_t t_bytes = p->use_tp ? p->tp_t_elems * 16 * (p->tp_overlap ? 2 : 1) : 0;
@@ -716,11 +750,11 @@ void build_plan(slsht_cuda_plan* p) {
     CK(cudaFuncSetAttribute(p->lines_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)p->couple_smem));
   } else if (p->use_tp) {
-    p->tp_gemm_smem = tgemm_smem_bytes(p->tp_KP, p->tp_bn);
-    p->tp_fft_smem = qfft_smem_bytes(p->n);
+    p->tp_gemm_smem = tgemm_smem_bytes(p->tp_KP, p->tp_bn, p->tp_gv == 1 ? 3 : 4);
+    p->tp_fft_smem = qfft_smem_bytes(p->n, p->tp_nt);
     p->couple_smem = std::max(p->tp_gemm_smem, p->tp_fft_smem);
-    CK(cudaFuncSetAttribute(p->tp_bn == 32 ? k_tgemm<32> : k_tgemm<64>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tp_gemm_smem));
+    CK(cudaFuncSetAttribute(tgemm_kernel(p->tp_gv), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)p->tp_gemm_smem));
     if (p->tp_overlap) {
       CK(cudaStreamCreateWithFlags(&p->fft_stream, cudaStreamNonBlocking));
       for (int i = 0; i < 2; ++i) {
@@ -979,7 +1013,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     tg.ncolp = p->tp_ncolp;
     tg.n = p->n;
     const dim3 tgrid((ch.count + TG_BM - 1) / TG_BM, p->tp_ncolp / p->tp_bn);
-    if (p->tp_bn == 32) {
+    if (p->tp_gv == 2) {
       // the GEMM of chunk i+1 is dispatched ahead of the FFT CTAs of chunk i (one GEMM CTA per
       // SM, one FFT CTA beside it)
       cudaLaunchConfig_t lc{};
@@ -994,10 +1028,12 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
       at[0].val.priority = hi;
       lc.attrs = at;
       lc.numAttrs = 1;
-      CK(cudaLaunchKernelEx(&lc, k_tgemm<32>, tg));
-    } else
-      k_tgemm<64><<<tgrid, tgemm_threads(64), p->tp_gemm_smem, s>>>(tg);
+      CK(cudaLaunchKernelEx(&lc, k_tgemm<32, 4, 1>, tg));
+    } else {
+      tgemm_kernel(p->tp_gv)<<<tgrid, tgemm_threads(p->tp_bn), p->tp_gemm_smem, s>>>(tg);
+    }
     CKL();
+    record(p, 5);
     cudaStream_t fs = s;
     if (overlap) {
       CK(cudaEventRecord(p->ev_tg[b], s));
@@ -1049,7 +1085,12 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   if (p->profile) {
     accumulate(p, ST_LEGENDRE, 0, 1);
     accumulate(p, ST_MODGEMM, 1, 2);
-    accumulate(p, ST_COUPLE, 2, 3);
+    if (p->use_tp) {
+      accumulate(p, ST_COUPLE, 2, 5);
+      accumulate(p, ST_QFFT, 5, 3);
+    } else {
+      accumulate(p, ST_COUPLE, 2, 3);
+    }
     accumulate(p, ST_DIGEST, 3, 4);
   }
 }
