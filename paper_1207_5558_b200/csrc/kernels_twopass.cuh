@@ -198,7 +198,8 @@ __host__ __device__ constexpr size_t qfft_smem_bytes(int n, int NT) {
 template <int N, int NT, int NTHR, int MINB>
 __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
   constexpr int L = (N - 1) / 2;
-  static_assert(NTHR % NT == 0, "threads must cover whole column sets");
+  // epilogue: (NTHR / NT) * NT threads own (column, row-set) pairs; the rest only reduce
+  static_assert(NTHR >= NT, "threads must cover the columns");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* Ts = reinterpret_cast<double2*>(smem_raw);
   double2* rou_s = Ts + N * NT;
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
   // epilogue: thread = (column cc, first row a_first); stores row by row (a warp writes 32
   // consecutive samples of one row), the mirror volume with sign flips, digest partials
   const int cc = tid % NT, col = col0 + cc;
-  const bool ok = col < P.ncol;
+  const bool ok = tid < (NTHR / NT) * NT && col < P.ncol;
   double s2 = 0.0, pr = 0.0, pi = 0.0, ir = 0.0, ii = 0.0, g0r = 0.0, g0i = 0.0;
   long long mx2 = 0;
   if (ok) {

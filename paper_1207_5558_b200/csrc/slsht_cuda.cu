@@ -313,14 +313,17 @@ TgemmFn tgemm_kernel(int v) {
   return v == 1 ? k_tgemm<32, 3, 2> : (v == 2 ? k_tgemm<32, 4, 1> : k_tgemm<64, 4, 1>);
 }
 
-// Two-pass coupling (kernels_twopass.cuh): the k_qfft instantiation per BASELINE length.
-// SLSHT_CUDA_QFFT=1 / 2 select the experimental shapes (96 threads; 16 columns x 64 threads).
+// Two-pass coupling (kernels_twopass.cuh): the k_qfft instantiation per BASELINE length
+// (n = 49, 65, 129; n = 17 and 33 keep their single-pass kernels).
+// SLSHT_CUDA_QFFT=1 / 2 / 3 select the experimental shapes (96 threads; 16 columns x 64
+// threads; 42 columns x 128 threads).
 bool tp_kernel(int n, void (*&fn)(QfParams), int& threads, int& nt) {
   const char* e = std::getenv("SLSHT_CUDA_QFFT");
   const int v = e ? std::atoi(e) : 0;
   threads = 128;
   nt = 32;
   switch (n) {
+    case 49: fn = k_qfft<49, 32, 128, 4>; break;
     case 65: fn = k_qfft<65, 32, 128, 4>; break;
     case 129:
       if (v == 1) {
@@ -330,6 +333,9 @@ bool tp_kernel(int n, void (*&fn)(QfParams), int& threads, int& nt) {
         fn = k_qfft<129, 16, 64, 4>;
         threads = 64;
         nt = 16;
+      } else if (v == 3) {  // 42 columns: 126 radix-43 butterflies on 128 threads
+        fn = k_qfft<129, 42, 128, 2>;
+        nt = 42;
       } else {
         fn = k_qfft<129, 32, 128, 2>;
       }
