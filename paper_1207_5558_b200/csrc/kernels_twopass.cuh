@@ -38,7 +38,7 @@ struct TgParams {
   int count, KP, ncolp, n;
 };
 
-__host__ __device__ constexpr int tgemm_threads(int BN) { return 64 * (BN / 16); }
+__host__ __device__ constexpr int tgemm_threads(int BN, int WNF) { return 64 * (BN / (8 * WNF)); }
 __host__ __device__ constexpr size_t tgemm_smem_bytes(int KP, int BN, int NST) {
   return (size_t)NST * (TG_BM * TG_ASTR + TG_KS * (BN + 2)) * 16 + (size_t)(KP / 4) * 2 + 16;
 }
@@ -49,12 +49,13 @@ __device__ __forceinline__ void st_global_v4(double2* p, double a, double b, dou
                : "memory");
 }
 
-// <64, 4, 1>: 8 warps, one CTA per SM. <32, 3, 2>: 4 warps, two independent CTAs per SM.
-// <32, 4, 1>: 4 warps (117 KB), which leaves room on the SM for one k_qfft CTA of the previous
-// chunk (the overlapped schedule).
-template <int BN, int TG_NST, int MINB>
-__global__ void __launch_bounds__(tgemm_threads(BN), MINB) k_tgemm(const TgParams P) {
-  constexpr int TG_THREADS = tgemm_threads(BN), TG_BSTR = BN + 2;
+// Warp tile 32 components x 8 WNF columns; BN columns per CTA, TG_NST pipeline stages.
+// <64, 2, 4, 1>: 8 warps, one CTA per SM. <32, 2, 3, 2>: 4 warps, two independent CTAs per SM.
+// <32, 2, 4, 1>: 4 warps (117 KB), which leaves room on the SM for one k_qfft CTA of the
+// previous chunk (the overlapped schedule). <32, 1, 3, 2>: 8 warps of 32 x 8.
+template <int BN, int WNF, int TG_NST, int MINB>
+__global__ void __launch_bounds__(tgemm_threads(BN, WNF), MINB) k_tgemm(const TgParams P) {
+  constexpr int TG_THREADS = tgemm_threads(BN, WNF), TG_BSTR = BN + 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As = reinterpret_cast<double2*>(smem_raw);
   double2* Bs = As + TG_NST * TG_BM * TG_ASTR;
@@ -92,22 +93,22 @@ __global__ void __launch_bounds__(tgemm_threads(BN), MINB) k_tgemm(const TgParam
   for (int s = 0; s < TG_NST - 1; ++s) load_stage(s);
 
   // warp tile: 32 components (4 MMA rows) x 16 columns (2 MMA columns)
-  constexpr int WN = BN / 16;
+  constexpr int WN = BN / (8 * WNF);
   const int wm = warp / WN, wn = warp % WN;
   const int arow = wm * 32 + (lane >> 2), acol = lane & 3;
-  const int brow = lane & 3, bcol = wn * 16 + (lane >> 2);
-  double c1[4][2][2], c2[4][2][2], c3[4][2][2];
+  const int brow = lane & 3, bcol = wn * 8 * WNF + (lane >> 2);
+  double c1[4][WNF][2], c2[4][WNF][2], c3[4][WNF][2];
   auto reset = [&]() {
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
+      for (int ni = 0; ni < WNF; ++ni)
 #pragma unroll
         for (int e = 0; e < 2; ++e) c1[mi][ni][e] = c2[mi][ni][e] = c3[mi][ni][e] = 0.0;
   };
   reset();
   const int scomp = comp0 + wm * 32 + (lane >> 2);
-  const int scol = col0 + wn * 16 + 2 * (lane & 3);
+  const int scol = col0 + wn * 8 * WNF + 2 * (lane & 3);
 
   for (int st = 0; st < nst; ++st) {
     cp_async_wait<TG_NST - 2>();
@@ -118,30 +119,30 @@ __global__ void __launch_bounds__(tgemm_threads(BN), MINB) k_tgemm(const TgParam
 #pragma unroll
     for (int kk = 0; kk < TG_KS / 4; ++kk) {
       const int ks = st * (TG_KS / 4) + kk;  // KP is a multiple of TG_KS: no partial stage
-      double2 a[4], b[2];
+      double2 a[4], b[WNF];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) a[mi] = Ab[(arow + mi * 8) * TG_ASTR + kk * 4 + acol];
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni) b[ni] = Bb[(kk * 4 + brow) * TG_BSTR + bcol + ni * 8];
+      for (int ni = 0; ni < WNF; ++ni) b[ni] = Bb[(kk * 4 + brow) * TG_BSTR + bcol + ni * 8];
       // Gauss: K1 += (ar+ai) br, K2 += ar (bi-br), K3 += ai (br+bi); re = K1-K3, im = K1+K2
-      double as[4], bd[2], bs[2];
+      double as[4], bd[WNF], bs[WNF];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) as[mi] = a[mi].x + a[mi].y;
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni) {
+      for (int ni = 0; ni < WNF; ++ni) {
         bd[ni] = b[ni].y - b[ni].x;
         bs[ni] = b[ni].x + b[ni].y;
       }
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
+      for (int ni = 0; ni < WNF; ++ni)
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) dmma(c1[mi][ni][0], c1[mi][ni][1], as[mi], b[ni].x);
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
+      for (int ni = 0; ni < WNF; ++ni)
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) dmma(c2[mi][ni][0], c2[mi][ni][1], a[mi].x, bd[ni]);
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
+      for (int ni = 0; ni < WNF; ++ni)
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) dmma(c3[mi][ni][0], c3[mi][ni][1], a[mi].y, bs[ni]);
       const int row = qend_s[ks];
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(tgemm_threads(BN), MINB) k_tgemm(const TgParam
           if (comp < P.count) {
             double2* dst = P.T + ((size_t)comp * P.n + row) * P.ncolp + scol;
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni)  // 32 B per lane: 4 lanes write one whole 128-B line
+            for (int ni = 0; ni < WNF; ++ni)  // 32 B per lane: 4 lanes write one whole 128-B line
               st_global_v4(dst + ni * 8, c1[mi][ni][0] - c3[mi][ni][0], c1[mi][ni][0] + c2[mi][ni][0],
                            c1[mi][ni][1] - c3[mi][ni][1], c1[mi][ni][1] + c2[mi][ni][1]);
           }
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(tgemm_threads(BN), MINB) k_tgemm(const TgParam
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni)
+        for (int ni = 0; ni < WNF; ++ni)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             c1[mi][ni][e] = row >= 0 ? 0.0 : c1[mi][ni][e];

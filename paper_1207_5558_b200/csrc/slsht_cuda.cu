@@ -121,7 +121,7 @@ struct slsht_cuda_plan {
   int tp_threads = 0;
   size_t tp_gemm_smem = 0, tp_fft_smem = 0;
   int tp_bn = 64;          //   k_tgemm column tile (32 in the overlapped schedule)
-  int tp_gv = 1;           //   k_tgemm variant: 0 <64,4,1>, 1 <32,3,2>, 2 <32,4,1>
+  int tp_gv = 1;           //   k_tgemm variant (tgemm_variant)
   bool tp_overlap = false; //   k_qfft + digest of chunk i on fft_stream under k_tgemm of i+1
   size_t tp_t_elems = 0;   //   one T buffer (two in the overlapped schedule)
   cudaStream_t fft_stream = nullptr;
@@ -309,22 +309,48 @@ bool ws_kernel(int n, WsKernel& k) {
 }
 
 using TgemmFn = void (*)(TgParams);
-TgemmFn tgemm_kernel(int v) {
-  return v == 1 ? k_tgemm<32, 3, 2> : (v == 2 ? k_tgemm<32, 4, 1> : k_tgemm<64, 4, 1>);
+// k_tgemm variants (SLSHT_CUDA_TGEMM): <BN, WNF, stages, CTAs per SM>
+struct TgemmVariant {
+  TgemmFn fn;
+  int bn, wnf, nst, per_sm;
+};
+TgemmVariant tgemm_variant(int v) {
+  switch (v) {
+    case 0: return {k_tgemm<64, 2, 4, 1>, 64, 2, 4, 1};
+    case 2: return {k_tgemm<32, 2, 4, 1>, 32, 2, 4, 1};
+    case 3: return {k_tgemm<32, 1, 3, 2>, 32, 1, 3, 2};
+    default: return {k_tgemm<32, 2, 3, 2>, 32, 2, 3, 2};
+  }
 }
 
 // Two-pass coupling (kernels_twopass.cuh): the k_qfft instantiation per BASELINE length
 // (n = 49, 65, 129; n = 17 and 33 keep their single-pass kernels).
-// SLSHT_CUDA_QFFT=1 / 2 / 3 select the experimental shapes (96 threads; 16 columns x 64
-// threads; 42 columns x 128 threads).
+// SLSHT_CUDA_QFFT=1 / 2 / 3 / 4 select the experimental shapes (96 threads; 16 columns x 64
+// threads; 42 columns x 128 threads; 64 columns x 256 threads).
 bool tp_kernel(int n, void (*&fn)(QfParams), int& threads, int& nt) {
   const char* e = std::getenv("SLSHT_CUDA_QFFT");
   const int v = e ? std::atoi(e) : 0;
   threads = 128;
   nt = 32;
   switch (n) {
-    case 49: fn = k_qfft<49, 32, 128, 4>; break;
-    case 65: fn = k_qfft<65, 32, 128, 4>; break;
+    case 49:
+      if (v == 4) {
+        fn = k_qfft<49, 64, 256, 2>;
+        threads = 256;
+        nt = 64;
+      } else {
+        fn = k_qfft<49, 32, 128, 4>;
+      }
+      break;
+    case 65:
+      if (v == 4) {
+        fn = k_qfft<65, 64, 256, 2>;
+        threads = 256;
+        nt = 64;
+      } else {
+        fn = k_qfft<65, 32, 128, 4>;
+      }
+      break;
     case 129:
       if (v == 1) {
         fn = k_qfft<129, 32, 96, 2>;
@@ -336,6 +362,10 @@ bool tp_kernel(int n, void (*&fn)(QfParams), int& threads, int& nt) {
       } else if (v == 3) {  // 42 columns: 126 radix-43 butterflies on 128 threads
         fn = k_qfft<129, 42, 128, 2>;
         nt = 42;
+      } else if (v == 4) {  // 64 columns (1-KB row segments), 256 threads, one CTA per SM
+        fn = k_qfft<129, 64, 256, 1>;
+        threads = 256;
+        nt = 64;
       } else {
         fn = k_qfft<129, 32, 128, 2>;
       }
@@ -392,8 +422,8 @@ void build_plan(slsht_cuda_plan* p) {
     // <64, 4, 1> (0) or <32, 4, 1> (2)
     const char* gv = std::getenv("SLSHT_CUDA_TGEMM");
     p->tp_gv = gv ? std::atoi(gv) : 1;
-    if (p->tp_gv < 0 || p->tp_gv > 2) p->tp_gv = 1;
-    p->tp_bn = p->tp_gv == 0 ? 64 : 32;
+    if (p->tp_gv < 0 || p->tp_gv > 3) p->tp_gv = 1;
+    p->tp_bn = tgemm_variant(p->tp_gv).bn;
   }
   // ---- component list: orders m (all or m >= 0 in real mode), degrees in the shard
   for (int m = p->real_mode ? 0 : -p->lmax; m <= p->lmax; ++m) {
@@ -427,7 +457,7 @@ void build_plan(slsht_cuda_plan* p) {
       int sms = 148;
       if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device) != cudaSuccess)
         sms = 148;
-      sms *= p->tp_gv == 1 ? 2 : 1;  // resident k_tgemm CTAs
+      sms *= tgemm_variant(p->tp_gv).per_sm;  // resident k_tgemm CTAs
       const long long nct = p->tp_ncolp / p->tp_bn, bmax = ch / TG_BM;
       long long best_b = bmax;
       double best = 0.0;
@@ -756,10 +786,10 @@ void build_plan(slsht_cuda_plan* p) {
     CK(cudaFuncSetAttribute(p->lines_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)p->couple_smem));
   } else if (p->use_tp) {
-    p->tp_gemm_smem = tgemm_smem_bytes(p->tp_KP, p->tp_bn, p->tp_gv == 1 ? 3 : 4);
+    p->tp_gemm_smem = tgemm_smem_bytes(p->tp_KP, p->tp_bn, tgemm_variant(p->tp_gv).nst);
     p->tp_fft_smem = qfft_smem_bytes(p->n, p->tp_nt);
     p->couple_smem = std::max(p->tp_gemm_smem, p->tp_fft_smem);
-    CK(cudaFuncSetAttribute(tgemm_kernel(p->tp_gv), cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(tgemm_variant(p->tp_gv).fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)p->tp_gemm_smem));
     if (p->tp_overlap) {
       CK(cudaStreamCreateWithFlags(&p->fft_stream, cudaStreamNonBlocking));
@@ -1024,7 +1054,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
       // SM, one FFT CTA beside it)
       cudaLaunchConfig_t lc{};
       lc.gridDim = tgrid;
-      lc.blockDim = dim3(tgemm_threads(32));
+      lc.blockDim = dim3(tgemm_threads(32, 2));
       lc.dynamicSmemBytes = p->tp_gemm_smem;
       lc.stream = s;
       cudaLaunchAttribute at[1];
@@ -1034,9 +1064,10 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
       at[0].val.priority = hi;
       lc.attrs = at;
       lc.numAttrs = 1;
-      CK(cudaLaunchKernelEx(&lc, k_tgemm<32, 4, 1>, tg));
+      CK(cudaLaunchKernelEx(&lc, k_tgemm<32, 2, 4, 1>, tg));
     } else {
-      tgemm_kernel(p->tp_gv)<<<tgrid, tgemm_threads(p->tp_bn), p->tp_gemm_smem, s>>>(tg);
+      const TgemmVariant tv = tgemm_variant(p->tp_gv);
+      tv.fn<<<tgrid, tgemm_threads(tv.bn, tv.wnf), p->tp_gemm_smem, s>>>(tg);
     }
     CKL();
     record(p, 5);
