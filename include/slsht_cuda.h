@@ -153,6 +153,15 @@ int slsht_cuda_inverse(slsht_cuda_plan* plan, const double* f, const double* h,
 int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int band_limit,
                                     int oversample, double* coeffs, double* lambda);
 
+/* forward_direct (transform.hpp:167-168, transform.cpp:313-388), the reference's independent
+ * direct engine, on the device: g(l, m; rho) = sh_analysis(sh_synthesis(f) sh_synthesis(R_rho h))
+ * on the sphere grid of band max(lmax, L_f + L_h), every component l <= lmax (lmax < 0: L_f +
+ * L_h) at the So3Volume cells `cells` (indices (a (L_h+1) + b)(2L_h+1) + c; NULL = every cell
+ * in order, ncells ignored). Host arrays; out: coeff_count(lmax) x ncells complex, row
+ * coeff_index(l, m), column = requested cell. Status codes as above. */
+int slsht_cuda_forward_direct(int device, int L_f, const double* f, int L_h, const double* h,
+                              int lmax, const long long* cells, long long ncells, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -193,6 +193,7 @@ class Reference(_Lib):
         L.ref_components.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_int, C.POINTER(C.c_int),
                                      C.POINTER(C.c_int), _dp]
         L.ref_rotate_coeffs.argtypes = [C.c_int, _dp, C.c_double, C.c_double, C.c_double, _dp]
+        L.ref_forward_direct.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_int, C.c_int, _dp]
 
     def delta_tables(self, L: int) -> np.ndarray:
         size = sum((2 * p + 1) ** 2 for p in range(L + 1))
@@ -288,6 +289,16 @@ class Reference(_Lib):
                                            _ptr(np.ascontiguousarray(h, dtype=np.complex128)),
                                            len(lm), ls, ms, _ptr(out)))
         return {k: out[i] for i, k in enumerate(lm)}
+
+    def forward_direct(self, f, L_f, h, L_h, lmax=-1, threads=0) -> np.ndarray:
+        """forward_direct (transform.cpp:313-388): [coeff_count(lmax), V] complex."""
+        lm = L_f + L_h if lmax < 0 else lmax
+        V = int(np.prod(volume_shape(L_h)))
+        out = np.zeros((coeff_count(lm), V), np.complex128)
+        f = np.ascontiguousarray(f, np.complex128)
+        h = np.ascontiguousarray(h, np.complex128)
+        self.check(self.lib.ref_forward_direct(L_f, _ptr(f), L_h, _ptr(h), lm, threads, _ptr(out)))
+        return out
 
     def eigenfunction_window(self, theta_c: float, a: float, L: int, oversample: int = 4):
         out = np.zeros(coeff_count(L), dtype=np.complex128)

@@ -255,6 +255,23 @@ int ref_components(int L_f, const double* f, int L_h, const double* h, int count
   });
 }
 
+// The reference's independent direct engine (transform.cpp:313-388): every component's
+// So3Volume, out[(coeff_index(l, m) * V + cell) * 2].
+int ref_forward_direct(int L_f, const double* f, int L_h, const double* h, int lmax, int threads,
+                       double* out) {
+  return guarded([&] {
+    const slsht::SphCoeffs fc = make_coeffs(L_f, f, 0);
+    const slsht::SphCoeffs hc = make_coeffs(L_h, h, 0);
+    slsht::ForwardOptions opts;
+    opts.lmax = lmax;
+    opts.threads = threads;
+    const slsht::SlshtDistribution d = slsht::forward_direct(fc, hc, opts);
+    const std::size_t V = static_cast<std::size_t>(2 * L_h + 1) * (2 * L_h + 1) * (L_h + 1);
+    for (std::size_t i = 0; i < d.components.size(); ++i)
+      std::memcpy(out + 2 * V * i, d.components[i].values.data(), sizeof(double) * 2 * V);
+  });
+}
+
 int ref_eigenfunction_window(double theta_c, double a, int L, int oversample,
                              double* out, double* lambda) {
   return guarded([&] {

@@ -40,6 +40,7 @@ EXPORTS = [
     "slsht_cuda_modulated",
     "slsht_cuda_inverse",
     "slsht_cuda_eigenfunction_window",
+    "slsht_cuda_forward_direct",
 ]
 
 
@@ -110,6 +111,9 @@ def load() -> C.CDLL:
     lib.slsht_cuda_eigenfunction_window.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int,
                                                     C.c_int, C.c_void_p, _dp]
     lib.slsht_cuda_eigenfunction_window.restype = C.c_int
+    lib.slsht_cuda_forward_direct.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
+                                              C.c_int, C.c_void_p, C.c_longlong, C.c_void_p]
+    lib.slsht_cuda_forward_direct.restype = C.c_int
     lib.slsht_cuda_modulated.argtypes = [C.c_void_p, C.c_void_p, C.c_int, _ip, _ip, _dp]
     lib.slsht_cuda_modulated.restype = C.c_int
     lib.slsht_cuda_inverse.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,

@@ -17,6 +17,7 @@
 #include "kernels_couple_ws.cuh"
 #include "kernels_couple_lines.cuh"
 #include "kernels_twopass.cuh"
+#include "direct.cuh"
 #include "window_solver.cuh"
 #include "kernels_setup.cuh"
 #include "slsht_cuda.h"
@@ -1620,6 +1621,208 @@ int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int ba
     cleanup();
     g_create_error = st.msg;
     return st.code;
+  }
+}
+
+// forward_direct (transform.cpp:313-388) on the device: direct.cuh. out[(l^2+l+m) * ncells + i]
+// is g(l, m) at cell cells[i] (every cell of the So3Volume in order when cells == NULL).
+int slsht_cuda_forward_direct(int device, int L_f, const double* f, int L_h, const double* h,
+                              int lmax, const long long* cells, long long ncells, double* out) {
+  std::vector<void*> allocs;
+  cublasHandle_t hb = nullptr;
+  cudaStream_t s = nullptr;
+  auto cleanup = [&]() {
+    if (hb) cublasDestroy(hb);
+    if (s) cudaStreamDestroy(s);
+    for (void* q : allocs) cudaFree(q);
+  };
+  try {
+    if (L_f < 0 || L_h < 0) throw Status{SLSHT_ERR_VALIDATION, "band limit must be non-negative"};
+    if (!f || !h || !out) throw Status{SLSHT_ERR_VALIDATION, "null argument"};
+    if (2 * L_h + 1 > 221)
+      throw Status{SLSHT_ERR_VALIDATION, "window band limit above 110 is not supported by this build"};
+    const int L_g = L_f + L_h;
+    if (lmax < 0) lmax = L_g;
+    const int L = std::max(lmax, L_g);  // sphere-grid band (transform.cpp:319)
+    const int n = 2 * L + 1, nt = L + 1, nh = 2 * L_h + 1, nb = L_h + 1, ncol = nh * nb;
+    const int NPQ = (L_h + 1) * (L_h + 1), NN = 2 * L + 1;  // colatitudes of S_{2L}
+    const long long vol = (long long)nh * ncol;
+    if (!cells) ncells = vol;
+    if (ncells <= 0) throw Status{SLSHT_ERR_VALIDATION, "no cells requested"};
+    int dev_count = 0;
+    if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+      throw Status{SLSHT_ERR_DEVICE, "no CUDA device available (the engine has no CPU fallback)"};
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CB(cublasCreate(&hb));
+    CB(cublasSetStream(hb, s));
+    auto dal = [&](size_t bytes) {
+      void* q = nullptr;
+      CK(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
+      allocs.push_back(q);
+      return q;
+    };
+    auto up = [&](const void* src, size_t bytes) {
+      void* d = dal(bytes);
+      CK(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s));
+      return d;
+    };
+    auto blocks = [](long long x, int b) { return (unsigned)((x + b - 1) / b); };
+    // ---- inputs, colatitudes, quadrature weights
+    const double2* d_f = (const double2*)up(f, 16 * (size_t)coeff_count(L_f));
+    const double* d_h = (const double*)up(h, 16 * (size_t)coeff_count(L_h));
+    std::vector<double> rings(nt), nodes(NN), wq = host_theta_weights(2 * L);
+    for (int t = 0; t < nt; ++t) rings[t] = kPi * (2 * t + 1) / n;            // grids.cpp:34-35
+    for (int j = 0; j < NN; ++j) nodes[j] = kPi * (2 * j + 1) / (4 * L + 1);  // harmonics.cpp:138
+    for (double& w : wq) w *= 2.0 * kPi;                                        // harmonics.cpp:164
+    const double* d_rings = (const double*)up(rings.data(), 8 * rings.size());
+    const double* d_nodes = (const double*)up(nodes.data(), 8 * nodes.size());
+    const double* d_wq = (const double*)up(wq.data(), 8 * wq.size());
+    // ---- t1 = the window table W[(p,q)][b n + c] (q-major (p,q) rows), from Delta and d(beta)
+    std::vector<int> pq(2 * NPQ), qoff(nh + 1, 0);
+    for (int jq = 0; jq < nh; ++jq) {
+      const int q = jq - L_h, aq = std::abs(q);
+      qoff[jq + 1] = qoff[jq] + (L_h + 1 - aq);
+      for (int pp = aq; pp <= L_h; ++pp) {
+        pq[2 * (qoff[jq] + pp - aq)] = q;
+        pq[2 * (qoff[jq] + pp - aq) + 1] = pp;
+      }
+    }
+    const int* d_pq = (const int*)up(pq.data(), 4 * pq.size());
+    std::vector<double2> rou(nh);
+    for (int k = 0; k < nh; ++k)
+      rou[k] = make_double2(std::cos(-2.0 * kPi * k / nh), std::sin(-2.0 * kPi * k / nh));
+    const double2* d_rou = (const double2*)up(rou.data(), 16 * rou.size());
+    size_t dsz = 0;
+    for (int pp = 0; pp <= L_h; ++pp) dsz += (size_t)(2 * pp + 1) * (2 * pp + 1);
+    double* d_delta = (double*)dal(8 * dsz);
+    double* d_dtab = (double*)dal(8 * dsz * nb);
+    double2* d_W = (double2*)dal(16 * (size_t)NPQ * ncol);
+    if (configure_delta(L_h) != cudaSuccess)
+      throw Status{SLSHT_ERR_VALIDATION, "window band limit too large for the on-chip Delta recursion"};
+    CK(launch_delta(L_h, d_delta, s));
+    const int wmax = nh * nh * nb;
+    k_dtab<<<dim3(blocks(wmax, 256), L_h + 1), 256, 0, s>>>(L_h, d_delta, d_rou, d_dtab);
+    CKL();
+    k_wtab<<<dim3(blocks(ncol, 128), NPQ), 128, 0, s>>>(L_h, d_h, d_dtab, d_rou, d_pq, 0, ncol,
+                                                       nullptr, d_W);
+    CKL();
+    // ---- synthesis tables: lambda_p^q(theta_t) in q-major (p,q) rows; F = sh_synthesis(f)
+    double* d_ls = (double*)dal(8 * (size_t)NPQ * nt);
+    for (int jq = 0; jq < nh; ++jq) {
+      const int q = jq - L_h;
+      k_dir_lrows<<<blocks(nt, 128), 128, 3 * (L_h + 2) * 8, s>>>(q, L_h, nt, d_rings, nullptr,
+                                                                 d_ls + (size_t)qoff[jq] * nt, nt);
+      CKL();
+    }
+    double2* d_fring = (double2*)dal(16 * (size_t)(2 * L_f + 1) * nt);
+    double2* d_F = (double2*)dal(16 * (size_t)nt * n);
+    k_dir_fring<<<dim3(blocks(nt, 128), 2 * L_f + 1), 128, 3 * (L_f + 2) * 8, s>>>(L_f, d_f, nt,
+                                                                                 d_rings, d_fring);
+    CKL();
+    k_dir_fmap<<<blocks((long long)nt * n, 128), 128, 0, s>>>(L_f, nt, n, d_fring, d_F);
+    CKL();
+    // ring DFTs: Esyn[k][q + L_h] = e^{+2 pi i q k / n}, Eana[m + L][k] = e^{-2 pi i m k / n} / n
+    double2* d_esyn = (double2*)dal(16 * (size_t)n * nh);
+    double2* d_eana = (double2*)dal(16 * (size_t)n * n);
+    k_dir_dft<<<blocks((long long)n * nh, 256), 256, 0, s>>>(n, nh, 0, -L_h, n, 1.0, 1.0, d_esyn);
+    CKL();
+    k_dir_dft<<<blocks((long long)n * n, 256), 256, 0, s>>>(n, n, -L, 0, n, -1.0, 1.0 / n, d_eana);
+    CKL();
+    // ---- analysis matrices Q_m = Lambda_m diag(2 pi v) B_{m mod 2}, rows l = |m|..lmax
+    double* d_B = (double*)dal(8 * 2 * (size_t)NN * nt);
+    k_dir_bpar<<<blocks((long long)NN * nt, 256), 256, 0, s>>>(L, NN, d_nodes, d_rings, d_B);
+    CKL();
+    std::vector<size_t> qm_off(2 * lmax + 2, 0);
+    for (int m = -lmax; m <= lmax; ++m)
+      qm_off[m + lmax + 1] = qm_off[m + lmax] + (size_t)(lmax - std::abs(m) + 1) * nt;
+    double* d_Q = (double*)dal(8 * qm_off.back());
+    double* d_la = (double*)dal(8 * (size_t)(lmax + 1) * NN);
+    const double one = 1.0, zero = 0.0;
+    for (int m = -lmax; m <= lmax; ++m) {
+      const int nl = lmax - std::abs(m) + 1;
+      k_dir_lrows<<<blocks(NN, 128), 128, 3 * (lmax + 2) * 8, s>>>(m, lmax, NN, d_nodes, d_wq, d_la,
+                                                                  NN);
+      CKL();
+      // row-major Q (nl x nt) = Lambda (nl x NN) B (NN x nt): column-major Q^T = B^T Lambda^T
+      CB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, nt, nl, NN, &one,
+                     d_B + (size_t)(m & 1) * NN * nt, nt, d_la, NN, &zero, d_Q + qm_off[m + lmax],
+                     nt));
+    }
+    // ---- cells in batches of R
+    const size_t per_r = 16 * ((size_t)NPQ + (size_t)nt * nh + 2 * (size_t)nt * n +
+                               (size_t)(2 * lmax + 1) * (lmax + 1) + (size_t)coeff_count(lmax)) +
+                         8;
+    const long long R = std::max<long long>(
+        1, std::min<long long>(ncells, (long long)((6ull << 30) / per_r)));
+    double2* d_HR = (double2*)dal(16 * (size_t)NPQ * R);
+    double2* d_S = (double2*)dal(16 * (size_t)nt * nh * R);
+    double2* d_H = (double2*)dal(16 * (size_t)nt * n * R);
+    double2* d_FM = (double2*)dal(16 * (size_t)nt * n * R);
+    double2* d_OUT = (double2*)dal(16 * (size_t)(2 * lmax + 1) * (lmax + 1) * R);
+    double2* d_res = (double2*)dal(16 * (size_t)coeff_count(lmax) * R);
+    long long* d_cells = (long long*)dal(8 * (size_t)R);
+    std::vector<long long> hcells(R);
+    const cuDoubleComplex zone = make_cuDoubleComplex(1.0, 0.0), zzero = make_cuDoubleComplex(0.0, 0.0);
+    for (long long c0 = 0; c0 < ncells; c0 += R) {
+      const int r = (int)std::min<long long>(R, ncells - c0);
+      for (int i = 0; i < r; ++i) {
+        hcells[i] = cells ? cells[c0 + i] : c0 + i;
+        if (hcells[i] < 0 || hcells[i] >= vol)
+          throw Status{SLSHT_ERR_VALIDATION, "cell index outside the So3Volume"};
+      }
+      CK(cudaMemcpyAsync(d_cells, hcells.data(), 8 * (size_t)r, cudaMemcpyHostToDevice, s));
+      k_dir_hr<<<dim3(blocks(r, 128), NPQ), 128, 0, s>>>(r, d_cells, NPQ, ncol, nh, d_pq, d_W, d_HR);
+      CKL();
+      // S[t][q][r] = sum_p lambda_p^q(theta_t) HR[(p,q)][r]  (real x complex: 2r real columns)
+      for (int jq = 0; jq < nh; ++jq) {
+        const int kq = qoff[jq + 1] - qoff[jq];
+        CB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, 2 * r, nt, kq, &one,
+                       reinterpret_cast<const double*>(d_HR + (size_t)qoff[jq] * r), 2 * r,
+                       d_ls + (size_t)qoff[jq] * nt, nt, &zero,
+                       reinterpret_cast<double*>(d_S + (size_t)jq * r), 2 * nh * r));
+      }
+      // H[t][k][r] = sum_q Esyn[k][q] S[t][q][r]
+      CB(cublasZgemmStridedBatched(hb, CUBLAS_OP_N, CUBLAS_OP_N, r, n, nh, &zone,
+                                   reinterpret_cast<const cuDoubleComplex*>(d_S), r,
+                                   (long long)nh * r,
+                                   reinterpret_cast<const cuDoubleComplex*>(d_esyn), nh, 0, &zzero,
+                                   reinterpret_cast<cuDoubleComplex*>(d_H), r, (long long)n * r, nt));
+      const long long tot = (long long)nt * n * r;
+      k_dir_product<<<blocks(tot, 256), 256, 0, s>>>(tot, r, d_F, d_H);
+      CKL();
+      // FM[t][m][r] = sum_k Eana[m][k] P[t][k][r]
+      CB(cublasZgemmStridedBatched(hb, CUBLAS_OP_N, CUBLAS_OP_N, r, n, n, &zone,
+                                   reinterpret_cast<const cuDoubleComplex*>(d_H), r,
+                                   (long long)n * r,
+                                   reinterpret_cast<const cuDoubleComplex*>(d_eana), n, 0, &zzero,
+                                   reinterpret_cast<cuDoubleComplex*>(d_FM), r, (long long)n * r, nt));
+      // OUT[m][l - |m|][r] = sum_t Q_m[l][t] FM[t][m][r]
+      for (int m = -lmax; m <= lmax; ++m) {
+        const int nl = lmax - std::abs(m) + 1;
+        CB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, 2 * r, nl, nt, &one,
+                       reinterpret_cast<const double*>(d_FM + (size_t)(m + L) * r), 2 * n * r,
+                       d_Q + qm_off[m + lmax], nt, &zero,
+                       reinterpret_cast<double*>(d_OUT + (size_t)(m + lmax) * (lmax + 1) * r),
+                       2 * r));
+      }
+      const long long nres = (long long)coeff_count(lmax) * r;
+      k_dir_scatter<<<blocks(nres, 256), 256, 0, s>>>(lmax, r, nres, d_OUT, d_res);
+      CKL();
+      CK(cudaMemcpy2DAsync(out + 2 * c0, 16 * (size_t)ncells, d_res, 16 * (size_t)r, 16 * (size_t)r,
+                           coeff_count(lmax), cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    cleanup();
+    return SLSHT_OK;
+  } catch (const Status& st) {
+    cleanup();
+    g_create_error = st.msg;
+    return st.code;
+  } catch (const CudaError& e) {
+    cleanup();
+    g_create_error = e.msg;
+    return SLSHT_ERR_DEVICE;
   }
 }
 

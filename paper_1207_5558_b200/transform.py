@@ -304,6 +304,31 @@ def eigenfunction_window(theta_c: float, a: float, band_limit: int, oversample: 
     return out, float(lam.value)
 
 
+def forward_direct(f: SphCoeffs, h: SphCoeffs, lmax: int = -1, cells=None,
+                   device: int = 0) -> np.ndarray:
+    """forward_direct (transform.cpp:313-388), the reference's independent direct engine, on the
+    device: g(l, m; rho) = sh_analysis(sh_synthesis(f) sh_synthesis(R_rho h)) on the sphere grid
+    of band max(lmax, L_g). Returns [coeff_count(lmax), cells] complex; `cells` are flat
+    So3Volume indices (a (L_h+1) + b)(2 L_h+1) + c (default: every cell, in volume order, so
+    row coeff_index(l, m) reshaped to volume_shape(L_h) is the component's So3Volume)."""
+    lib = L.load()
+    lm = f.band_limit + h.band_limit if lmax < 0 else int(lmax)
+    fa = np.ascontiguousarray(f.data, np.complex128)
+    ha = np.ascontiguousarray(h.data, np.complex128)
+    if cells is None:
+        ncell = int(np.prod(volume_shape(h.band_limit)))
+        cptr = None
+    else:
+        cells = np.ascontiguousarray(cells, np.int64)
+        ncell = int(cells.size)
+        cptr = cells.ctypes.data
+    out = np.zeros((coeff_count(lm), ncell), np.complex128)
+    rc = lib.slsht_cuda_forward_direct(device, f.band_limit, fa.ctypes.data, h.band_limit,
+                                       ha.ctypes.data, lm, cptr, ncell, out.ctypes.data)
+    _raise(rc, None)
+    return out
+
+
 def modulated_sht(f: SphCoeffs, lm: list[tuple[int, int]], window_band_limit: int,
                   device: int = 0) -> np.ndarray:
     """ModulatedSht::compute for several (l, m): [len(lm), coeff_count(L_h)] complex."""

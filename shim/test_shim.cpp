@@ -35,6 +35,8 @@ void reference_forward_fast(const SphCoeffs& f, const SphCoeffs& h, const Compon
                             const ForwardOptions& opts);
 SlshtDistribution reference_forward_fast(const SphCoeffs& f, const SphCoeffs& h,
                                          const ForwardOptions& opts);
+SlshtDistribution reference_forward_direct(const SphCoeffs& f, const SphCoeffs& h,
+                                           const ForwardOptions& opts);
 // the reference's CPU window solver, renamed at compile time (see Makefile)
 Window reference_eigenfunction_window(const EllipticalRegion& region, int band_limit,
                                       int oversample);
@@ -71,6 +73,21 @@ static double max_diff(const SlshtDistribution& a, const SlshtDistribution& b) {
 }
 
 int main() {
+  {
+    // forward_direct drop-in (the device direct engine) against the reference's CPU direct
+    // engine, and against the fast engine
+    const SphCoeffs f = random_complex(6, 45), h = random_complex(3, 46);
+    const SlshtDistribution a = forward_direct(f, h);
+    const SlshtDistribution b = reference_forward_direct(f, h, {});
+    report(max_diff(a, b) < 1e-12, "forward_direct (6, 3) vs reference forward_direct",
+           max_diff(a, b), 1e-12);
+    ForwardOptions lo;
+    lo.lmax = 4;
+    const double d2 = max_diff(forward_direct(f, h, lo), reference_forward_direct(f, h, lo));
+    report(d2 < 1e-12, "forward_direct lmax = 4 < L_g vs reference", d2, 1e-12);
+    const double d3 = max_diff(a, forward_fast(f, h));
+    report(d3 < 1e-12, "forward_direct vs forward_fast (6, 3)", d3, 1e-12);
+  }
   {
     const SphCoeffs f = random_complex(3, 41), h = random_complex(2, 42);
     report(max_diff(forward_fast(f, h), reference_forward_fast(f, h, {})) < 1e-12,

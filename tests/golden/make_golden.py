@@ -5,7 +5,7 @@ Run in a container where /root/reference exists (`make -C oracle ref` first):
     python tests/golden/make_golden.py
 Every array here comes from the reference's own code path (forward_fast, the component-level
 ModulatedSht / build_c_tensor / So3Evaluator chain of proj/src/cli.cpp:94-143, DeltaTables,
-theta_weights, legendre_rows, InverseAccumulator); inputs are either stored or regenerated
+theta_weights, legendre_rows, InverseAccumulator, forward_direct); inputs are either stored or regenerated
 deterministically by paper_1207_5558_b200.configs (their checksums are stored).
 """
 from __future__ import annotations
@@ -160,8 +160,25 @@ def make_roundtrip() -> None:
     print("roundtrip.npz")
 
 
+def make_direct() -> None:
+    # the reference's independent direct engine forward_direct (transform.cpp:313-388): full
+    # distributions of small cases (lmax = L_g, lmax < L_g, lmax > L_g: sphere band lmax)
+    arrays = {}
+    for name, L_f, L_h, lmax, seed in (("a", 6, 3, -1, 61), ("b", 9, 4, 5, 62), ("c", 3, 2, 7, 63)):
+        f = random_complex(L_f, seed)
+        h = synthetic_window(L_h, seed + 100)
+        arrays[f"{name}_f"] = f
+        arrays[f"{name}_h"] = h
+        arrays[f"{name}_meta"] = np.array([L_f, L_h, lmax])
+        arrays[f"{name}_g"] = R.forward_direct(f, L_f, h, L_h, lmax)
+    np.savez_compressed(OUT / "direct.npz", **arrays)
+    print("direct.npz")
+
+
 def main() -> None:
-    which = set(sys.argv[1:]) or {"tables", "small", "1", "2", "3", "4", "5", "rt"}
+    which = set(sys.argv[1:]) or {"tables", "small", "1", "2", "3", "4", "5", "rt", "direct"}
+    if "direct" in which:
+        make_direct()
     if "tables" in which:
         make_tables()
     if "small" in which:
