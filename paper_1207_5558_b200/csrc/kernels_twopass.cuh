@@ -52,7 +52,7 @@ __device__ __forceinline__ void st_global_v4(double2* p, double a, double b, dou
 // Warp tile 32 components x 8 WNF columns; BN columns per CTA, TG_NST pipeline stages.
 // <64, 2, 4, 1>: 8 warps, one CTA per SM. <32, 2, 3, 2>: 4 warps, two independent CTAs per SM.
 // <32, 2, 4, 1>: 4 warps (117 KB), which leaves room on the SM for one k_qfft CTA of the
-// previous chunk (the overlapped schedule). <32, 1, 3, 2>: 8 warps of 32 x 8.
+// previous chunk (the overlapped schedule).
 template <int BN, int WNF, int TG_NST, int MINB>
 __global__ void __launch_bounds__(tgemm_threads(BN, WNF), MINB) k_tgemm(const TgParams P) {
   constexpr int TG_THREADS = tgemm_threads(BN, WNF), TG_BSTR = BN + 2;

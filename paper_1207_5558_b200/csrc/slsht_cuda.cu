@@ -319,58 +319,21 @@ TgemmVariant tgemm_variant(int v) {
   switch (v) {
     case 0: return {k_tgemm<64, 2, 4, 1>, 64, 2, 4, 1};
     case 2: return {k_tgemm<32, 2, 4, 1>, 32, 2, 4, 1};
-    case 3: return {k_tgemm<32, 1, 3, 2>, 32, 1, 3, 2};
     default: return {k_tgemm<32, 2, 3, 2>, 32, 2, 3, 2};
   }
 }
 
 // Two-pass coupling (kernels_twopass.cuh): the k_qfft instantiation per BASELINE length
 // (n = 49, 65, 129; n = 17 and 33 keep their single-pass kernels).
-// SLSHT_CUDA_QFFT=1 / 2 / 3 / 4 select the experimental shapes (96 threads; 16 columns x 64
-// threads; 42 columns x 128 threads; 64 columns x 256 threads).
 bool tp_kernel(int n, void (*&fn)(QfParams), int& threads, int& nt) {
-  const char* e = std::getenv("SLSHT_CUDA_QFFT");
-  const int v = e ? std::atoi(e) : 0;
+  // one component x 32 columns per CTA, 128 threads (k_qfft<129> shapes tried and not kept:
+  // 96 threads, 16 x 64, 42 x 128, 64 x 256, three CTAs per SM)
   threads = 128;
   nt = 32;
   switch (n) {
-    case 49:
-      if (v == 4) {
-        fn = k_qfft<49, 64, 256, 2>;
-        threads = 256;
-        nt = 64;
-      } else {
-        fn = k_qfft<49, 32, 128, 4>;
-      }
-      break;
-    case 65:
-      if (v == 4) {
-        fn = k_qfft<65, 64, 256, 2>;
-        threads = 256;
-        nt = 64;
-      } else {
-        fn = k_qfft<65, 32, 128, 4>;
-      }
-      break;
-    case 129:
-      if (v == 1) {
-        fn = k_qfft<129, 32, 96, 2>;
-        threads = 96;
-      } else if (v == 2) {
-        fn = k_qfft<129, 16, 64, 4>;
-        threads = 64;
-        nt = 16;
-      } else if (v == 3) {  // 42 columns: 126 radix-43 butterflies on 128 threads
-        fn = k_qfft<129, 42, 128, 2>;
-        nt = 42;
-      } else if (v == 4) {  // 64 columns (1-KB row segments), 256 threads, one CTA per SM
-        fn = k_qfft<129, 64, 256, 1>;
-        threads = 256;
-        nt = 64;
-      } else {
-        fn = k_qfft<129, 32, 128, 2>;
-      }
-      break;
+    case 49: fn = k_qfft<49, 32, 128, 4>; break;
+    case 65: fn = k_qfft<65, 32, 128, 4>; break;
+    case 129: fn = k_qfft<129, 32, 128, 2>; break;
     default: return false;
   }
   return true;
@@ -423,7 +386,7 @@ void build_plan(slsht_cuda_plan* p) {
     // <64, 4, 1> (0) or <32, 4, 1> (2)
     const char* gv = std::getenv("SLSHT_CUDA_TGEMM");
     p->tp_gv = gv ? std::atoi(gv) : 1;
-    if (p->tp_gv < 0 || p->tp_gv > 3) p->tp_gv = 1;
+    if (p->tp_gv < 0 || p->tp_gv > 2) p->tp_gv = 1;
     p->tp_bn = tgemm_variant(p->tp_gv).bn;
   }
   // ---- component list: orders m (all or m >= 0 in real mode), degrees in the shard
