@@ -122,7 +122,7 @@ struct slsht_cuda_plan {
   int tp_threads = 0;
   size_t tp_gemm_smem = 0, tp_fft_smem = 0;
   int tp_bn = 64;          //   k_tgemm column tile (32 in the overlapped schedule)
-  int tp_gv = 1;           //   k_tgemm variant (tgemm_variant)
+  int tp_gv = 3;           //   k_tgemm variant (tgemm_variant)
   bool tp_overlap = false; //   k_qfft + digest of chunk i on fft_stream under k_tgemm of i+1
   size_t tp_t_elems = 0;   //   one T buffer (two in the overlapped schedule)
   cudaStream_t fft_stream = nullptr;
@@ -319,6 +319,7 @@ TgemmVariant tgemm_variant(int v) {
   switch (v) {
     case 0: return {k_tgemm<64, 2, 4, 1>, 64, 2, 4, 1};
     case 2: return {k_tgemm<32, 2, 4, 1>, 32, 2, 4, 1};
+    case 3: return {k_tgemm<32, 2, 2, 3>, 32, 2, 2, 3};
     default: return {k_tgemm<32, 2, 3, 2>, 32, 2, 3, 2};
   }
 }
@@ -330,9 +331,10 @@ bool tp_kernel(int n, void (*&fn)(QfParams), int& threads, int& nt) {
   // 96 threads, 16 x 64, 42 x 128, 64 x 256, three CTAs per SM)
   threads = 128;
   nt = 32;
+  // CTAs per SM: 6 (n = 49), 5 (n = 65) measured best (4 or 8 / 6 slower: DESIGN.md §7)
   switch (n) {
-    case 49: fn = k_qfft<49, 32, 128, 4>; break;
-    case 65: fn = k_qfft<65, 32, 128, 4>; break;
+    case 49: fn = k_qfft<49, 32, 128, 6>; break;
+    case 65: fn = k_qfft<65, 32, 128, 5>; break;
     case 129: fn = k_qfft<129, 32, 128, 2>; break;
     default: return false;
   }
@@ -382,11 +384,11 @@ void build_plan(slsht_cuda_plan* p) {
     p->use_tp = !(e && e[0] == '0') && tp_kernel(p->n, p->tp_fft, p->tp_threads, p->tp_nt);
     p->tp_ncolp = (p->ncol + TG_BN - 1) / TG_BN * TG_BN;
     p->tp_ntiles = (p->ncol + p->tp_nt - 1) / p->tp_nt;
-    // k_tgemm shape: <32, 3, 2> (two 4-warp CTAs per SM) unless SLSHT_CUDA_TGEMM selects
-    // <64, 4, 1> (0) or <32, 4, 1> (2)
+    // k_tgemm shape: <32, 2, 2, 3> (three 4-warp CTAs per SM, two stages) unless
+    // SLSHT_CUDA_TGEMM selects <64, 2, 4, 1> (0), <32, 2, 3, 2> (1) or <32, 2, 4, 1> (2)
     const char* gv = std::getenv("SLSHT_CUDA_TGEMM");
-    p->tp_gv = gv ? std::atoi(gv) : 1;
-    if (p->tp_gv < 0 || p->tp_gv > 2) p->tp_gv = 1;
+    p->tp_gv = gv ? std::atoi(gv) : 3;
+    if (p->tp_gv < 0 || p->tp_gv > 3) p->tp_gv = 3;
     p->tp_bn = tgemm_variant(p->tp_gv).bn;
   }
   // ---- component list: orders m (all or m >= 0 in real mode), degrees in the shard
