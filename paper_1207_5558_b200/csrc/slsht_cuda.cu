@@ -717,7 +717,7 @@ void build_plan(slsht_cuda_plan* p) {
   if (p->use_tp) {
     const char* e = std::getenv("SLSHT_CUDA_TP_OVERLAP");
     p->tp_overlap = p->chunks.size() > 1 && e && e[0] == '1';  // measured slower: opt-in
-    if (p->tp_overlap) {
+    if (p->tp_overlap && !std::getenv("SLSHT_CUDA_TGEMM")) {
       p->tp_gv = 2;
       p->tp_bn = 32;
     }
