@@ -37,7 +37,6 @@ struct CoupleParams {
   const double* betaw;
   FftPlan fft;
   int generic_dft;  // runtime path: n has a prime factor above kMaxGeneratedRadix
-  int group_major;  // grid x = component group (CTAs in flight share one W column tile)
 };
 
 constexpr int smallest_prime_factor(int n) {
@@ -203,8 +202,8 @@ __global__ void __launch_bounds__(NTHR, MINB) k_couple(const CoupleParams P) {
   int* perm_s = reinterpret_cast<int*>(betaw_s + (L + 1));
   int* qoff_s = perm_s + n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ct = P.group_major ? blockIdx.y : blockIdx.x;
-  const int comp0 = (P.group_major ? blockIdx.x : blockIdx.y) * MT;
+  const int ct = blockIdx.x;
+  const int comp0 = blockIdx.y * MT;
   const int col0 = ct * NT;
   for (int i = tid; i < n; i += NTHR) {
     rou_s[i] = P.rou[i];

@@ -931,7 +931,6 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   prm.betaw = p->d_betaw;
   prm.fft = p->fft;
   prm.generic_dft = p->generic_dft;
-  prm.group_major = std::getenv("SLSHT_CUDA_GROUP_MAJOR") != nullptr;
   const int MT = 8 * p->MG;
   if (p->use_lines) {
     LnParams lp{};
@@ -1073,7 +1072,6 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     p->launches += 1;
   } else {
     dim3 grid(p->n_col_tiles, (ch.count + MT - 1) / MT);
-    if (prm.group_major) grid = dim3((ch.count + MT - 1) / MT, p->n_col_tiles);
     couple_kernel(p->n, p->MG, p->NG)<<<grid, couple_threads(p->n), p->couple_smem, s>>>(prm);
   }
   CKL();
