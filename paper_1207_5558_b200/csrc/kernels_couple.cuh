@@ -48,8 +48,9 @@ constexpr int smallest_prime_factor(int n) {
 // One DIF stage of radix R on sub-transforms of span S (compile-time N), executed by the
 // NTHR threads numbered tid = 0..NTHR-1. SINK: the twiddle-free last stage of a radix with a
 // streaming butterfly (Radix<R>::dft_sink) stores each output as soon as it is formed.
-template <int N, int R, int S, int NT, int PAIRS, int NTHR, bool SINK = false>
+template <int N, int R, int S, int NT, int PAIRS, int NTHR, bool SINK = false, int TS = NT>
 __device__ __forceinline__ void fft_stage_ct(double2* T, const double2* rou_s, int tid) {
+  // TS: row stride of the tile in shared memory (NT unless padded against bank conflicts)
   constexpr int MP = S / R;
   constexpr int TOTAL = PAIRS * (N / R);
   double xr[R], xi[R];
@@ -58,16 +59,16 @@ __device__ __forceinline__ void fft_stage_ct(double2* T, const double2* rou_s, i
     const int bfl = item / PAIRS;
     const int blk = bfl / MP, t = bfl % MP;
     const int comp = pair / NT, col = pair % NT;
-    double2* base = T + (size_t)(comp * N + blk * S + t) * NT + col;
+    double2* base = T + (size_t)(comp * N + blk * S + t) * TS + col;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      const double2 v = base[k * MP * NT];
+      const double2 v = base[k * MP * TS];
       xr[k] = v.x;
       xi[k] = v.y;
     }
     if constexpr (SINK && MP == 1 && R >= kSinkMinRadix) {
       Radix<R>::dft_sink(xr, xi, [&](int k, double yr, double yi) {
-        base[k * NT] = make_double2(yr, yi);
+        base[k * TS] = make_double2(yr, yi);
       });
       continue;
     }
@@ -75,12 +76,12 @@ __device__ __forceinline__ void fft_stage_ct(double2* T, const double2* rou_s, i
     base[0] = make_double2(xr[0], xi[0]);
     if (MP == 1 || t == 0) {
 #pragma unroll
-      for (int k = 1; k < R; ++k) base[k * MP * NT] = make_double2(xr[k], xi[k]);
+      for (int k = 1; k < R; ++k) base[k * MP * TS] = make_double2(xr[k], xi[k]);
     } else {
 #pragma unroll
       for (int k = 1; k < R; ++k) {
         const double2 w = rou_s[t * k * (N / S)];
-        base[k * MP * NT] = make_double2(xr[k] * w.x - xi[k] * w.y, xr[k] * w.y + xi[k] * w.x);
+        base[k * MP * TS] = make_double2(xr[k] * w.x - xi[k] * w.y, xr[k] * w.y + xi[k] * w.x);
       }
     }
   }

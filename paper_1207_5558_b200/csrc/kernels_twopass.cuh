@@ -178,6 +178,145 @@ __global__ void __launch_bounds__(tgemm_threads(BN, WNF), MINB) k_tgemm(const Tg
 }
 
 // ---------------------------------------------------------------------------------------------
+// Last DIF stage of N = 3 x 43 (k_qfft<129>) on the FP64 tensor cores. For each of the 3 NT
+// length-43 sub-transforms (GEMM column n = blk NT + c), X_k = sum_j x_j w^{jk} in the
+// symmetric form
+//   X_k = (x0r + P1 + P3, x0i + P2 - P4),  X_{43-k} = (x0r + P1 - P3, x0i + P2 + P4),
+//   P1 = C SR, P2 = C SI, P3 = S DI, P4 = S DR,  C_kj = cos(2 pi jk / 43), S_kj = sin(...),
+// with s_j = x_j + x_{43-j}, d_j = x_j - x_{43-j} (j = 1..21) formed in place first. The four
+// (k = 0..23) x (j = 1..24, zero-padded) by (j) x (8 columns) products of an 8-column tile are
+// DMMA 8x8x4 chains; a warp owns its tiles' columns, so it writes the outputs in place. Same
+// FP64 work as the scalar butterflies, but ~140 registers instead of 255 and every warp busy.
+// A fragments of the cos / sin matrices, [cos|sin][mt < 3][ks < 6][lane]: row k = mt 8 + lane/4,
+// column j = ks 4 + lane%4 + 1 (zero for j > 21 or k > 21). Filled once per plan.
+__global__ void k_r43_table(double* __restrict__ tab) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * 6 * 32) return;
+  const int lane = i % 32, ks = (i / 32) % 6, mt = i / 192;
+  const int k = mt * 8 + (lane >> 2), j = ks * 4 + (lane & 3) + 1;
+  double sn = 0.0, cs = 0.0;
+  if (j <= 21 && k <= 21) sincospi(2.0 * (double)((j * k) % 43) / 43.0, &sn, &cs);
+  tab[i] = cs;
+  tab[576 + i] = sn;
+}
+
+// First DIF stage of N = 129 (radix 3 with twiddles, as fft_stage_ct) fused with the sums and
+// differences of the radix-43 stage: a thread takes the stage-1 items t and 43 - t of a column
+// together, so every sub-transform's s_j, d_j land in place without another pass.
+template <int NT, int TS, int NTHR>
+__device__ __forceinline__ void radix3_with_sums(double2* T, const double2* rou_s, int tid) {
+  constexpr int R = 43, H = 21;
+  for (int e = tid; e < NT * (H + 1); e += NTHR) {
+    const int c = e % NT, t = e / NT;  // t = 0: the x_0 rows; t = 1..21: the pairs (t, 43 - t)
+    double yr[2][3], yi[2][3];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int u = h ? R - t : t;
+      if (h && t == 0) break;
+      double2* base = T + (size_t)u * TS + c;
+      double xr[3], xi[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double2 v = base[k * R * TS];
+        xr[k] = v.x;
+        xi[k] = v.y;
+      }
+      Radix<3>::dft(xr, xi);
+      yr[h][0] = xr[0];
+      yi[h][0] = xi[0];
+#pragma unroll
+      for (int k = 1; k < 3; ++k) {
+        if (u == 0) {
+          yr[h][k] = xr[k];
+          yi[h][k] = xi[k];
+        } else {
+          const double2 w = rou_s[u * k];
+          yr[h][k] = xr[k] * w.x - xi[k] * w.y;
+          yi[h][k] = xr[k] * w.y + xi[k] * w.x;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {  // sub-transform k: rows k 43 + j
+      double2* col = T + (size_t)(k * R) * TS + c;
+      if (t == 0) {
+        col[0] = make_double2(yr[0][k], yi[0][k]);
+      } else {
+        col[t * TS] = make_double2(yr[0][k] + yr[1][k], yi[0][k] + yi[1][k]);
+        col[(R - t) * TS] = make_double2(yr[0][k] - yr[1][k], yi[0][k] - yi[1][k]);
+      }
+    }
+  }
+}
+
+template <int NT, int TS, int NTHR>
+__device__ __forceinline__ void radix43_dmma(double2* T, int tid, const double* __restrict__ tab) {
+  // TS: tile row stride; TS == 2 (mod 8) keeps the 4 rows of a B fragment in distinct banks.
+  // Expects rows j / 43 - j of every sub-transform to hold s_j / d_j (radix3_with_sums).
+  constexpr int R = 43, H = 21, NTILE = 3 * NT / 8, NW = NTHR / 32;
+  static_assert(NT % 8 == 0, "a column tile must stay inside one sub-transform");
+  const int lane = tid & 31, warp = tid >> 5;
+  double ca[3][6], sa[3][6];  // A fragments (k_r43_table)
+#pragma unroll
+  for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < 6; ++ks) {
+      ca[mt][ks] = __ldg(tab + (mt * 6 + ks) * 32 + lane);
+      sa[mt][ks] = __ldg(tab + 576 + (mt * 6 + ks) * 32 + lane);
+    }
+  for (int nt = warp; nt < NTILE; nt += NW) {
+    double pp[4][3][2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int mt = 0; mt < 3; ++mt) pp[q][mt][0] = pp[q][mt][1] = 0.0;
+    const int nb = nt * 8 + (lane >> 2);  // B fragment column
+    const double2* colb = T + (size_t)((nb / NT) * R) * TS + nb % NT;
+#pragma unroll
+    for (int ks = 0; ks < 6; ++ks) {
+      const int j = ks * 4 + (lane & 3) + 1;
+      double2 sv = make_double2(0.0, 0.0), dv = make_double2(0.0, 0.0);
+      if (j <= H) {
+        sv = colb[j * TS];
+        dv = colb[(R - j) * TS];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 3; ++mt) {
+        dmma(pp[0][mt][0], pp[0][mt][1], ca[mt][ks], sv.x);
+        dmma(pp[1][mt][0], pp[1][mt][1], ca[mt][ks], sv.y);
+        dmma(pp[2][mt][0], pp[2][mt][1], sa[mt][ks], dv.y);
+        dmma(pp[3][mt][0], pp[3][mt][1], sa[mt][ks], dv.x);
+      }
+    }
+    // outputs: lane holds k = mt 8 + lane/4 of columns n = nt 8 + 2 (lane%4) + e
+    double2 x0[2];
+    double2* colo[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int n = nt * 8 + 2 * (lane & 3) + e;
+      colo[e] = T + (size_t)((n / NT) * R) * TS + n % NT;
+      x0[e] = colo[e][0];
+    }
+    __syncwarp();  // every lane read its x_0 (and its B fragments) before any write
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int mt = 0; mt < 3; ++mt) {
+        const int k = mt * 8 + (lane >> 2);
+        if (k > H) continue;
+        const double p1 = pp[0][mt][e], p2 = pp[1][mt][e], p3 = pp[2][mt][e], p4 = pp[3][mt][e];
+        if (k == 0) {
+          colo[e][0] = make_double2(x0[e].x + p1, x0[e].y + p2);
+        } else {
+          colo[e][k * TS] = make_double2(x0[e].x + p1 + p3, x0[e].y + p2 - p4);
+          colo[e][(R - k) * TS] = make_double2(x0[e].x + p1 - p3, x0[e].y + p2 + p4);
+        }
+      }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // k_qfft: one component x NT grid columns per CTA.
 
 struct QfParams {
@@ -191,10 +330,14 @@ struct QfParams {
   const double2* rou;
   const int* perm;
   const double* betaw;
+  const double* r43;  // k_r43_table (n = 129)
 };
 
+// row stride of the k_qfft tile: padded to == 2 (mod 8) for the DMMA radix-43 stage (n = 129)
+__host__ __device__ constexpr int qfft_row_stride(int n, int NT) { return n == 129 ? NT + 2 : NT; }
 __host__ __device__ constexpr size_t qfft_smem_bytes(int n, int NT) {
-  return (size_t)n * NT * 16 + (size_t)n * 16 + (size_t)((n + 1) / 2) * 8 + (size_t)n * 4 + 64;
+  return (size_t)n * qfft_row_stride(n, NT) * 16 + (size_t)n * 16 + (size_t)((n + 1) / 2) * 8 +
+         (size_t)n * 4 + 64;
 }
 
 template <int N, int NT, int NTHR, int MINB>
@@ -204,7 +347,8 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
   static_assert(NTHR >= NT, "threads must cover the columns");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* Ts = reinterpret_cast<double2*>(smem_raw);
-  double2* rou_s = Ts + N * NT;
+  constexpr int TS = qfft_row_stride(N, NT);  // tile row stride
+  double2* rou_s = Ts + N * TS;
   double* betaw_s = reinterpret_cast<double*>(rou_s + N);
   int* perm_s = reinterpret_cast<int*>(betaw_s + (L + 1));
   const int tid = threadIdx.x;
@@ -219,14 +363,22 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
     const double2* src = P.T + (size_t)comp * N * P.ncolp + col0;
     for (int e = tid; e < N * NT; e += NTHR) {
       const int row = e / NT, c = e % NT;
-      cp_async16(Ts + e, src + (size_t)row * P.ncolp + c, true);
+      cp_async16(Ts + row * TS + c, src + (size_t)row * P.ncolp + c, true);
     }
     cp_async_commit();
   }
   cp_async_wait<0>();
   __syncthreads();
 
-  FftDif<N, N, NT, NT, NTHR, true>::run(Ts, rou_s, tid, 0);
+  if constexpr (N == 129) {
+    radix3_with_sums<NT, TS, NTHR>(Ts, rou_s, tid);
+    __syncthreads();
+    radix43_dmma<NT, TS, NTHR>(Ts, tid, P.r43);
+    __syncthreads();
+  } else {
+    static_assert(TS == NT, "the generic DIF plan assumes an unpadded tile");
+    FftDif<N, N, NT, NT, NTHR, true>::run(Ts, rou_s, tid, 0);
+  }
 
   // epilogue: thread = (column cc, first row a_first); stores row by row (a warp writes 32
   // consecutive samples of one row), the mirror volume with sign flips, digest partials
@@ -247,7 +399,7 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
     uint32_t hsh = (uint32_t)((size_t)a_first * P.ncol + col) * 0x9E3779B1u;
     const uint32_t hstep = (uint32_t)((size_t)A_STEP * P.ncol) * 0x9E3779B1u;
     if (a_first == 0 && col == 0) {
-      const double2 t = Tp[(size_t)perm_s[0] * NT];
+      const double2 t = Tp[(size_t)perm_s[0] * TS];
       g0r = t.x;
       g0i = t.y;
     }
@@ -255,7 +407,7 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
       constexpr bool MIR = decltype(mirror_tag)::value;
 #pragma unroll 4
       for (int a = a_first; a < N; a += A_STEP, hsh += hstep) {
-        const double2 t = Tp[(size_t)perm_s[a] * NT];
+        const double2 t = Tp[(size_t)perm_s[a] * TS];
         const double vr = t.x, vi = t.y;
         const size_t idx = (size_t)a * P.ncol;
         __stcs(o + idx, make_double2(vr, vi));

@@ -172,6 +172,7 @@ struct slsht_cuda_plan {
   double2* d_T = nullptr;   // two-pass: T of one chunk
   short* d_qend = nullptr;  // two-pass: per k-step, the T row it completes (or -1)
   int* d_wrow = nullptr;    // two-pass: W row of every (p, q)
+  double* d_r43 = nullptr;  // two-pass, n = 129: DMMA fragments of the radix-43 stage
   double2* d_out = nullptr;
   double* d_partials = nullptr;
   double* d_digest = nullptr;
@@ -195,6 +196,7 @@ void free_plan(slsht_cuda_plan* p) {
   cudaFree(p->d_T);
   cudaFree(p->d_qend);
   cudaFree(p->d_wrow);
+  cudaFree(p->d_r43);
   cudaFree(p->d_h);
   cudaFree(p->d_ncos);
   cudaFree(p->d_nsin);
@@ -328,14 +330,14 @@ TgemmVariant tgemm_variant(int v) {
 // (n = 49, 65, 129; n = 17 and 33 keep their single-pass kernels).
 bool tp_kernel(int n, void (*&fn)(QfParams), int& threads, int& nt) {
   // one component x 32 columns per CTA, 128 threads (k_qfft<129> shapes tried and not kept:
-  // 96 threads, 16 x 64, 42 x 128, 64 x 256, three CTAs per SM)
+  // 96 threads, 16 x 64, 42 x 128, 64 x 256)
   threads = 128;
   nt = 32;
   // CTAs per SM: 6 (n = 49), 5 (n = 65) measured best (4 or 8 / 6 slower: DESIGN.md §7)
   switch (n) {
     case 49: fn = k_qfft<49, 32, 128, 6>; break;
     case 65: fn = k_qfft<65, 32, 128, 5>; break;
-    case 129: fn = k_qfft<129, 32, 128, 2>; break;
+    case 129: fn = k_qfft<129, 32, 128, 3>; break;  // radix-43 stage on DMMA: 168 registers
     default: return false;
   }
   return true;
@@ -682,6 +684,11 @@ void build_plan(slsht_cuda_plan* p) {
     CK(cudaMemsetAsync(p->d_W, 0, (size_t)p->tp_KP * p->tp_ncolp * 16, s));  // padding rows
     p->d_wrow = dupload(wrow, s);
     p->d_qend = dupload(qend, s);
+    if (p->n == 129) {
+      p->d_r43 = dalloc<double>(2 * 576);
+      k_r43_table<<<3, 192, 0, s>>>(p->d_r43);
+      CKL();
+    }
   } else {
     p->d_W = dalloc<double2>((size_t)p->NPQ * ncol_pad);
   }
@@ -1057,6 +1064,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     qf.rou = p->d_rou;
     qf.perm = p->d_perm;
     qf.betaw = p->d_betaw;
+    qf.r43 = p->d_r43;
     p->tp_fft<<<dim3(p->tp_ntiles, ch.count), p->tp_threads, p->tp_fft_smem, fs>>>(qf);
     CKL();
     if (overlap) {
