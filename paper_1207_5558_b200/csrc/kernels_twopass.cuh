@@ -38,9 +38,11 @@ struct TgParams {
   int count, KP, ncolp, n;
 };
 
-__host__ __device__ constexpr int tgemm_threads(int BN, int WNF) { return 64 * (BN / (8 * WNF)); }
-__host__ __device__ constexpr size_t tgemm_smem_bytes(int KP, int BN, int NST) {
-  return (size_t)NST * (TG_BM * TG_ASTR + TG_KS * (BN + 2)) * 16 + (size_t)(KP / 4) * 2 + 16;
+__host__ __device__ constexpr int tgemm_threads(int BN, int WNF, int BM = TG_BM) {
+  return 32 * (BM / 32) * (BN / (8 * WNF));
+}
+__host__ __device__ constexpr size_t tgemm_smem_bytes(int KP, int BN, int NST, int BM = TG_BM) {
+  return (size_t)NST * (BM * TG_ASTR + TG_KS * (BN + 2)) * 16 + (size_t)(KP / 4) * 2 + 16;
 }
 
 // 256-bit global store (sm_100): two consecutive complex values
@@ -54,27 +56,27 @@ __device__ __forceinline__ void st_global_v4(double2* p, double a, double b, dou
 // <64, 2, 4, 1>: 8 warps, one CTA per SM. <32, 2, 3, 2>: 4 warps, two CTAs per SM.
 // <32, 2, 4, 1>: 4 warps (117 KB), which leaves room on the SM for one k_qfft CTA of the
 // previous chunk (the overlapped schedule).
-template <int BN, int WNF, int TG_NST, int MINB>
-__global__ void __launch_bounds__(tgemm_threads(BN, WNF), MINB) k_tgemm(const TgParams P) {
-  constexpr int TG_THREADS = tgemm_threads(BN, WNF), TG_BSTR = BN + 2;
+template <int BN, int WNF, int TG_NST, int MINB, int BM = TG_BM>
+__global__ void __launch_bounds__(tgemm_threads(BN, WNF, BM), MINB) k_tgemm(const TgParams P) {
+  constexpr int TG_THREADS = tgemm_threads(BN, WNF, BM), TG_BSTR = BN + 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As = reinterpret_cast<double2*>(smem_raw);
-  double2* Bs = As + TG_NST * TG_BM * TG_ASTR;
+  double2* Bs = As + TG_NST * BM * TG_ASTR;
   short* qend_s = reinterpret_cast<short*>(Bs + TG_NST * TG_KS * TG_BSTR);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // grid x = component block: the CTAs in flight share a few W column tiles (read from HBM
   // once per chunk) while the chunk's U stays L2-resident
-  const int comp0 = blockIdx.x * TG_BM, col0 = blockIdx.y * BN;
+  const int comp0 = blockIdx.x * BM, col0 = blockIdx.y * BN;
   const int nks = P.KP / 4, nst = (P.KP + TG_KS - 1) / TG_KS;
   for (int i = tid; i < nks; i += TG_THREADS) qend_s[i] = P.qend[i];
 
   auto load_stage = [&](int st) {
     if (st < nst) {
       const int kb = st * TG_KS;
-      double2* Ad = As + (st % TG_NST) * TG_BM * TG_ASTR;
+      double2* Ad = As + (st % TG_NST) * BM * TG_ASTR;
       double2* Bd = Bs + (st % TG_NST) * TG_KS * TG_BSTR;
 #pragma unroll
-      for (int j = 0; j < TG_BM * TG_KS / TG_THREADS; ++j) {
+      for (int j = 0; j < BM * TG_KS / TG_THREADS; ++j) {
         const int e = tid + j * TG_THREADS;
         const int c = e / TG_KS, k = e % TG_KS;
         const bool ok = comp0 + c < P.count && kb + k < P.KP;
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(tgemm_threads(BN, WNF), MINB) k_tgemm(const Tg
     cp_async_wait<TG_NST - 2>();
     __syncthreads();
     load_stage(st + TG_NST - 1);  // refills the buffer consumed at st - 1 (all warps passed it)
-    const double2* Ab = As + (st % TG_NST) * TG_BM * TG_ASTR;
+    const double2* Ab = As + (st % TG_NST) * BM * TG_ASTR;
     const double2* Bb = Bs + (st % TG_NST) * TG_KS * TG_BSTR;
 #pragma unroll
     for (int kk = 0; kk < TG_KS / 4; ++kk) {

@@ -315,14 +315,14 @@ using TgemmFn = void (*)(TgParams);
 // k_tgemm variants (SLSHT_CUDA_TGEMM): <BN, WNF, stages, CTAs per SM>
 struct TgemmVariant {
   TgemmFn fn;
-  int bn, wnf, nst, per_sm;
+  int bn, wnf, nst, per_sm, bm;
 };
 TgemmVariant tgemm_variant(int v) {
   switch (v) {
-    case 0: return {k_tgemm<64, 2, 4, 1>, 64, 2, 4, 1};
-    case 2: return {k_tgemm<32, 2, 4, 1>, 32, 2, 4, 1};
-    case 3: return {k_tgemm<32, 2, 2, 3>, 32, 2, 2, 3};
-    default: return {k_tgemm<32, 2, 3, 2>, 32, 2, 3, 2};
+    case 0: return {k_tgemm<64, 2, 4, 1>, 64, 2, 4, 1, 64};
+    case 2: return {k_tgemm<32, 2, 4, 1>, 32, 2, 4, 1, 64};
+    case 3: return {k_tgemm<32, 2, 2, 3>, 32, 2, 2, 3, 64};
+    default: return {k_tgemm<32, 2, 3, 2>, 32, 2, 3, 2, 64};
   }
 }
 
@@ -759,7 +759,8 @@ void build_plan(slsht_cuda_plan* p) {
     CK(cudaFuncSetAttribute(p->lines_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)p->couple_smem));
   } else if (p->use_tp) {
-    p->tp_gemm_smem = tgemm_smem_bytes(p->tp_KP, p->tp_bn, tgemm_variant(p->tp_gv).nst);
+    p->tp_gemm_smem = tgemm_smem_bytes(p->tp_KP, p->tp_bn, tgemm_variant(p->tp_gv).nst,
+                                       tgemm_variant(p->tp_gv).bm);
     p->tp_fft_smem = qfft_smem_bytes(p->n, p->tp_nt);
     p->couple_smem = std::max(p->tp_gemm_smem, p->tp_fft_smem);
     CK(cudaFuncSetAttribute(tgemm_variant(p->tp_gv).fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1020,7 +1021,8 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     tg.KP = p->tp_KP;
     tg.ncolp = p->tp_ncolp;
     tg.n = p->n;
-    const dim3 tgrid((ch.count + TG_BM - 1) / TG_BM, p->tp_ncolp / p->tp_bn);
+    const int tbm = tgemm_variant(p->tp_gv).bm;
+    const dim3 tgrid((ch.count + tbm - 1) / tbm, p->tp_ncolp / p->tp_bn);
     if (p->tp_gv == 2) {
       // the GEMM of chunk i+1 is dispatched ahead of the FFT CTAs of chunk i (one GEMM CTA per
       // SM, one FFT CTA beside it)
@@ -1039,7 +1041,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
       CK(cudaLaunchKernelEx(&lc, k_tgemm<32, 2, 4, 1>, tg));
     } else {
       const TgemmVariant tv = tgemm_variant(p->tp_gv);
-      tv.fn<<<tgrid, tgemm_threads(tv.bn, tv.wnf), p->tp_gemm_smem, s>>>(tg);
+      tv.fn<<<tgrid, tgemm_threads(tv.bn, tv.wnf, tv.bm), p->tp_gemm_smem, s>>>(tg);
     }
     CKL();
     record(p, 5);
