@@ -1796,6 +1796,10 @@ int slsht_cuda_forward_direct(int device, int L_f, const double* f, int L_h, con
     cleanup();
     g_create_error = e.msg;
     return SLSHT_ERR_DEVICE;
+  } catch (const std::exception& e) {  // host allocation of the tables / cell lists
+    cleanup();
+    g_create_error = e.what();
+    return SLSHT_ERR_DEVICE;
   }
 }
 
