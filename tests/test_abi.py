@@ -74,6 +74,9 @@ def test_validation_precedes_device_checks():
     h = S.SphCoeffs(1, np.zeros(4))
     with pytest.raises(S.ValidationError):
         S.forward_fast(f, h, opts=S.ForwardOptions(lmax=5))
+    with pytest.raises(S.ValidationError):  # band limits are checked before the device
+        S.forward_direct(S.SphCoeffs(2, np.zeros(9)), S.SphCoeffs(111, np.zeros(112 * 112)),
+                         cells=[0])
 
 
 @pytest.mark.skipif(_cuda_available(), reason="checks the no-GPU error path")
@@ -84,6 +87,8 @@ def test_no_cpu_fallback_without_gpu():
         S.Plan(4, 2)
     with pytest.raises(S.DeviceError):
         S.delta_tables(4)
+    with pytest.raises(S.DeviceError, match="no CPU fallback"):  # the direct engine too
+        S.forward_direct(S.SphCoeffs(2, np.zeros(9)), S.SphCoeffs(1, np.zeros(4)))
 
 
 def test_product_never_imports_the_oracle():
