@@ -433,12 +433,14 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
     ir *= qb;
     ii *= qb;
   }
-  // fixed-order reduction: a shuffle tree per warp, then the warps in order
-  double v[8] = {s2, __longlong_as_double(mx2), pr, pi, g0r, g0i, ir, ii};
+  // fixed-order reduction: a shuffle tree per warp, then the warps in order. g000 is held by
+  // thread 0 of the first column tile alone (a = 0, column 0), so it is written, not reduced.
+  // digest fields reduced: 0..3 (s2, max, pr, pi) and 6, 7 (ir, ii)
+  double v[6] = {s2, __longlong_as_double(mx2), pr, pi, ir, ii};
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 6; ++k) {
       const double o = __shfl_down_sync(0xffffffffu, v[k], off);
       v[k] = (k == 1) ? fmax(v[k], o) : v[k] + o;
     }
@@ -446,15 +448,20 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
   double* red = reinterpret_cast<double*>(smem_raw);
   if ((tid & 31) == 0)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) red[(tid >> 5) * 8 + k] = v[k];
+    for (int k = 0; k < 6; ++k) red[(tid >> 5) * 6 + k] = v[k];
   __syncthreads();
-  if (tid < 8) {
+  double* part = P.partials + ((size_t)comp * P.n_tiles + ct) * 8;
+  if (tid < 6) {
     double acc = 0.0;
     for (int w = 0; w < NTHR / 32; ++w) {
-      const double x = red[w * 8 + tid];
+      const double x = red[w * 6 + tid];
       acc = (tid == 1) ? fmax(acc, x) : acc + x;
     }
-    P.partials[((size_t)comp * P.n_tiles + ct) * 8 + tid] = acc;
+    part[tid < 4 ? tid : tid + 2] = acc;
+  }
+  if (tid == 0) {
+    part[4] = g0r;
+    part[5] = g0i;
   }
 }
 
