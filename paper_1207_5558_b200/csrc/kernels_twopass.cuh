@@ -2,18 +2,18 @@
 //
 //   k_tgemm  T[comp][q mod n][col] = sum_{p>=|q|} U[comp][(p,q)] W[(p,q)][col]
 //            one batched complex GEMM per q on the FP64 tensor cores (DMMA 8x8x4, Gauss
-//            3-product), 64 components x 64 columns per CTA, every q of the tile in one pass
-//            over the q-major (p, q) rows (each q padded to whole k-steps of 4), operands
-//            staged in shared memory by a 4-deep cp.async ring. T goes to an HBM buffer.
+//            3-product), 64 components x 32 columns per CTA (three CTAs per SM), every q of the
+//            tile in one pass over the q-major (p, q) rows (each q padded to whole k-steps of
+//            4), operands staged in shared memory by a cp.async ring. T goes to an HBM buffer.
 //   k_qfft   reads T[comp][*][32 columns], runs the length-n alpha DIF FFT in shared memory
-//            (fft_radix.cuh butterflies, the plan of k_couple) and writes the So3Volume rows
-//            (and the real-mode mirror) with the digest partials.
+//            (fft_radix.cuh butterflies; for n = 129 the radix-43 stage on the tensor cores)
+//            and writes the So3Volume rows (and the real-mode mirror) with the digest partials.
 //
 // Why two passes: the single-pass k_couple must keep all n rows of its T tile on chip, which
 // caps its tile at 8 components x 8 columns for n = 129 (132 KB); each operand byte then
 // feeds only 8 MACs, and the DMMA loop runs L2-bound at ~16% of the tensor pipe
-// (profiles/r01_ncu_couple_c5_*.txt). The T round trip costs 32 B of extra HBM traffic per
-// sample, but lets the GEMM run on 64x64 tiles (8x the operand reuse).
+// (profiles/r01_ncu_couple_c5_singlepass.txt). The T round trip costs 32 B of extra HBM
+// traffic per sample, but frees the GEMM tile (8x the operand reuse).
 #pragma once
 
 #include <type_traits>
