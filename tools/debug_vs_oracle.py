@@ -1,4 +1,4 @@
-"""GPU volumes vs the C oracle for one (L_f, L_h, lmax, real) case: python tools/debug_blk.py L_f L_h lmax [real]"""
+"""GPU volumes vs the C oracle for one (L_f, L_h, lmax, real) case: python tools/debug_vs_oracle.py L_f L_h lmax [real]"""
 import sys
 import numpy as np
 sys.path.insert(0, '/root/repo')
