@@ -3,17 +3,21 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
-A step is one complete forward_fast of BASELINE config C (default 2 = configs[1]) on seeded
-synthetic inputs: setup tables (Delta, d(beta), window table, I-table, theta weights), every
-computed component (Legendre rows, modulated-SHT GEMM, coupling + alpha FFT) and the fused
-epilogue that writes every emitted volume (mirrors included) to device memory and digests it.
+A step is one complete forward_fast of BASELINE config C (default 4 = configs[3], the largest
+configuration that runs on one GPU; config 5 is the 8-GPU scaling config) on seeded synthetic
+inputs: setup tables (Delta, d(beta), window table, I-table, theta weights), every computed
+component (Legendre rows, modulated-SHT GEMM, coupling + alpha FFT) and the fused epilogue that
+writes every emitted volume (mirrors included) to device memory and digests it.
 
-value  : emitted samples g(rho; l, m) per second, whole job, inputs resident in HBM,
-         CUDA events on the engine stream, max over ranks (N > 1: degrees sharded by l).
+value  : emitted samples g(rho; l, m) per second, whole job, inputs resident in HBM, CUDA events
+         on the engine stream, max over ranks (N > 1: degrees sharded by l).
 e2e    : the same through the C ABI with HOST buffers: H2D of f, h and D2H of the per-component
          digests inside the timed region, host wall clock around the synchronous call.
-Rank 0 prints ONE JSON line. `--impl reference` times the reference's own CPU forward_fast
-(oracle/_ref, unmodified sources) on the host cores instead.
+Rank 0 prints ONE JSON line. With --gpus N > 1 and no WORLD_SIZE in the environment, bench.py
+launches its N ranks itself (torch.distributed.run, 127.0.0.1). `--impl reference` times the
+reference's own CPU forward_fast (oracle/_ref, the unmodified sources) on the host cores, with
+the SURVEY.md §8(d) recipe (full runs for configs 1-2, setup-separated extrapolation of a sampled
+run for configs 3-5).
 """
 from __future__ import annotations
 
@@ -21,6 +25,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,16 +39,21 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"]
-P_FP64_TFLOPS = 37.1  # measured DMMA peak on this pool's B200 (profiles/fp64_peak.txt)
-CPU_SAMPLE_LMAX = {1: 40, 2: 48, 3: 40, 4: 30, 5: 12}
+# builder-measured DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peak.txt); not in
+# MEASURED_PEAKS.json, which has no FP64 entry
+P_FP64_TFLOPS = 37.1
+FP64_SOURCE = "builder-measured DMMA m8n8k4 burst peak (profiles/fp64_peak.txt)"
+# sampled lmax of the CPU reference for configs 3-5 (configs 1-2 run in full), SURVEY.md §8(d)
+CPU_SAMPLE_LMAX = {3: 32, 4: 32, 5: 12}
+L2_NOTE = "256 MiB L2 flush between timed GPU steps (outside the event pairs)"
 
 
 def load_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "source": "measured"}
-    return {"hbm_gbs": 6650.0, "source": "fallback"}
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "source": "measured (MEASURED_PEAKS.json hbm_gbs)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
 class ClockSampler:
@@ -66,6 +76,7 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            time.sleep(0.2)  # the first sample lands inside the timed region
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -113,71 +124,163 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def reference_sample(cfg_index: int, steps: int, warmup: int, threads: int) -> dict:
-    """The reference's CPU forward_fast (oracle/_ref) on a bounded sample of the workload:
-    forward_fast(f, h, digest-sink, opts.lmax = L_s) with SLSHT threads = host cores."""
-    import oracle
-    from paper_1207_5558_b200 import configs as C
-
-    R = oracle.Reference()
-    f, h, cfg = C.make_inputs(cfg_index)
-    ls = CPU_SAMPLE_LMAX[cfg_index]
-    times = []
-    for i in range(warmup + steps):
-        _, secs = R.forward_fast_digest(f, cfg.L_f, cfg.f_real, h, cfg.L_h, cfg.h_real, lmax=ls,
-                                        threads=threads)
-        if i >= warmup:
-            times.append(secs)
-    samples = cfg.samples(ls)
-    t = statistics.median(times)
+def workload_config(cfg, world: int) -> dict:
+    """The `config` object, identical in both arms (the driver compares them)."""
     return {
-        "value": samples / t,
-        "seconds_per_step": t,
-        "samples_per_step": samples,
-        "sample": (f"config {cfg_index} forward_fast with opts.lmax={ls} "
-                   f"({cfg.computed(ls)} computed / {cfg.emitted(ls)} emitted components of "
-                   f"{cfg.computed()} / {cfg.emitted()}; per-component cost is independent of l), "
-                   f"digest sink under the reference mutex, median of {len(times)}"),
-        "cores": threads,
-        "cpu": cpu_model(),
+        "workload": (f"config{cfg.index}: forward_fast L_f={cfg.L_f} L_h={cfg.L_h} "
+                     f"{'real-mode' if cfg.real_mode else 'full-m'} ({cfg.description})"),
+        "L_f": cfg.L_f, "L_h": cfg.L_h, "real_mode": cfg.real_mode,
+        "samples_per_step": cfg.samples(),
+        "computed_components": cfg.computed(), "emitted_components": cfg.emitted(),
+        "l2": L2_NOTE,
+        "parallelism": f"l-shard x{world}",
     }
+
+
+# ------------------------------------------------------------------------ reference (CPU) arm
+class ReferenceTimer:
+    """The reference's CPU forward_fast (oracle/_ref, unmodified sources, -O3) with a digest
+    sink under its own mutex, on `threads` host threads:
+      configs 1-2: the full call per step;
+      configs 3-5: forward_fast with opts.lmax = L_s per step, extrapolated as
+        T = T_setup + (T_run - T_setup) * N_full / N_sample,
+      T_setup = ModulatedSht + DeltaTables + So3Evaluator (transform.cpp:256-258, serial),
+      median of 3, timed once; per-component cost is independent of l."""
+
+    def __init__(self, cfg_index: int, threads: int):
+        import oracle
+        from paper_1207_5558_b200 import configs as C
+
+        self.R = oracle.Reference()
+        self.f, self.h, self.cfg = C.make_inputs(cfg_index)
+        self.threads = threads
+        self.ls = CPU_SAMPLE_LMAX.get(cfg_index)  # None: full runs
+        self.t_setup = None
+        if self.ls is not None:
+            cfg = self.cfg
+            self.t_setup = statistics.median(
+                self.R.setup_seconds(self.f, cfg.L_f, cfg.f_real, self.h, cfg.L_h, cfg.h_real)
+                for _ in range(3))
+
+    def run(self) -> tuple[float, float]:
+        """One step: (measured seconds, seconds of the full forward_fast (extrapolated))."""
+        cfg = self.cfg
+        _, secs = self.R.forward_fast_digest(self.f, cfg.L_f, cfg.f_real, self.h, cfg.L_h,
+                                             cfg.h_real, lmax=-1 if self.ls is None else self.ls,
+                                             threads=self.threads)
+        if self.ls is None:
+            return secs, secs
+        scale = cfg.computed() / cfg.computed(self.ls)
+        return secs, self.t_setup + max(secs - self.t_setup, 0.0) * scale
+
+    def sample_text(self, steps: int) -> str:
+        cfg = self.cfg
+        if self.ls is None:
+            return (f"config {cfg.index} full forward_fast ({cfg.computed()} computed / "
+                    f"{cfg.emitted()} emitted components), digest sink under the reference "
+                    f"mutex, median of {steps}")
+        return (f"config {cfg.index} forward_fast with opts.lmax={self.ls} ({cfg.computed(self.ls)}"
+                f" of {cfg.computed()} computed components), digest sink; extrapolated "
+                f"T = T_setup + (T_run - T_setup) * {cfg.computed()}/{cfg.computed(self.ls)} with "
+                f"T_setup = {self.t_setup:.3f} s (ModulatedSht + DeltaTables + So3Evaluator, "
+                f"serial, median of 3); median of {steps} steps")
 
 
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
-        return
+        return  # the CPU reference runs once, on rank 0
     from paper_1207_5558_b200 import configs as C
 
     cfg = C.CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     threads = os.cpu_count() or 1
     try:
-        r = reference_sample(args.config, args.steps, args.warmup, threads)
+        rt = ReferenceTimer(args.config, threads)
+        for _ in range(args.warmup):
+            rt.run()
+        meas, full = [], []
+        for _ in range(args.steps):
+            a, b = rt.run()
+            meas.append(a)
+            full.append(b)
     except Exception as e:  # the reference library is always built with the repo
         print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}))
         return
+    t_full = statistics.median(full)
+    value = cfg.samples() / t_full
+    kind = "reference"
     line = {
         "impl": "reference",
         "metric": METRIC,
-        "value": r["value"],
+        "value": value,
         "unit": "samples/s",
         "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": r["seconds_per_step"] * 1e3,
+        "ms_per_step": statistics.mean(meas) * 1e3,
+        "ms_per_full_run": t_full * 1e3,
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded BASELINE recipe)",
-        "config": {"workload": f"config{args.config}", "L_f": cfg.L_f, "L_h": cfg.L_h,
-                   "real_mode": cfg.real_mode, "samples_per_step": r["samples_per_step"]},
-        "cpu_baseline": {"value": r["value"], "unit": "samples/s", "cores": r["cores"],
-                         "kind": "reference", "sample": r["sample"], "cpu": r["cpu"]},
-        "e2e": {"value": r["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
+        "data": "synthetic (seeded BASELINE recipe; Slepian windows solved by the reference)",
+        "config": workload_config(cfg, world),
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": kind,
+                         "sample": rt.sample_text(args.steps), "cpu": cpu_model(),
+                         "extrapolated": rt.ls is not None},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+
+
+# ------------------------------------------------------------------------ our arm
+def spawn_ranks(args) -> int:
+    """--gpus N without an external launcher: run N ranks through torch.distributed.run."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def roundtrip_error(dig: np.ndarray, f: np.ndarray, h: np.ndarray, cfg) -> float:
+    """max|f_rec - f| / max|f| with f_rec(l, m) = integrate_volume(g(l, m)) / (sqrt(16 pi^3) h00)
+    for l <= L_f (inverse_slsht / InverseAccumulator, transform.cpp:469-540), from the digest
+    epilogue's quadrature integrals (fields 6, 7) of every emitted component."""
+    rows = (cfg.L_f + 1) ** 2
+    rec = (dig[:rows, 6] + 1j * dig[:rows, 7]) / (math.sqrt(16.0 * math.pi ** 3) * h[0])
+    return float(np.max(np.abs(rec - f)) / np.max(np.abs(f)))
+
+
+def host_sink_sample(S, C, cfg, f_np, h_np, dev: int, budget_bytes: float = 2.5e9) -> dict:
+    """Host-sink throughput: slsht_cuda_forward (pinned, double-buffered D2H) into the library's
+    copy sink (the materializing forward_fast's copy into host memory) over a degree range of
+    about `budget_bytes` of output (the full config does not fit in host memory)."""
+    vol_bytes = cfg.volume * 16
+    target = max(1, int(budget_bytes // vol_bytes))
+    l1 = cfg.L_g + 1
+    l0 = l1
+    while l0 > 0 and l1 * l1 - l0 * l0 < target:
+        l0 -= 1
+    rows = l1 * l1 - l0 * l0
+    out = np.empty((rows,) + S.volume_shape(cfg.L_h), np.complex128)
+    out.reshape(-1)[:: max(1, out.size // 1024)] = 0  # touch a little; pages fault in the copy
+    with S.Plan(cfg.L_f, cfg.L_h, real_mode=cfg.real_mode, emit_negative_m=True, device=dev,
+                l_begin=l0, l_end=l1, ring_bytes=1 << 30) as plan:
+        plan.forward_copy(f_np, h_np, out, first_index=l0 * l0)  # warm-up (faults the pages in)
+        t0 = time.perf_counter()
+        delivered, dropped = plan.forward_copy(f_np, h_np, out, first_index=l0 * l0)
+        secs = time.perf_counter() - t0
+    samples = delivered * cfg.volume
+    return {"value": samples / secs, "unit": "samples/s", "gb_per_s": samples * 16 / secs / 1e9,
+            "degrees": [l0, l1], "components": delivered, "dropped": dropped,
+            "how": ("slsht_cuda_forward + slsht_cuda_copy_sink into host memory (the "
+                    "materializing forward_fast's copy), degrees [l0, l1) of the config, wall "
+                    "clock, second call")}
 
 
 def run_ours(args) -> None:
@@ -190,6 +293,8 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} does not match --gpus {args.gpus}")
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
@@ -206,7 +311,8 @@ def run_ours(args) -> None:
     # inputs resident in HBM (torch is only the allocator here)
     f_dev = torch.from_numpy(f_np.view(np.float64).copy()).to(dev)
     h_dev = torch.from_numpy(h_np.view(np.float64).copy()).to(dev)
-    dig_dev = torch.zeros((S.coeff_count(cfg.L_g), S.DIGEST_WIDTH), dtype=torch.float64, device=dev)
+    dig_dev = torch.full((S.coeff_count(cfg.L_g), S.DIGEST_WIDTH), float("nan"),
+                         dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step():
@@ -215,7 +321,7 @@ def run_ours(args) -> None:
                             synchronize=False)
 
     my_samples = plan.emitted_count * plan.volume_elems
-    single_chunk = materialize  # one chunk: per-step stage events are live in the graph
+    single_chunk = materialize  # one chunk: per-step kernel events are live in the graph
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -228,7 +334,7 @@ def run_ours(args) -> None:
     torch.cuda.synchronize(dev)
     with ClockSampler(local) as clocks:
         t_wall = time.perf_counter()
-        live_stages = []
+        live = []
         for i in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.fill_(i & 0xFF)  # L2 flush between steps, outside the event pair
@@ -239,15 +345,19 @@ def run_ours(args) -> None:
                 # the step's own coupling-kernel events (recorded around the kernel on the
                 # engine stream, inside its CUDA graph); read after the step's event pair
                 evs[i][1].synchronize()
-                live_stages.append(plan.kernel_time())
+                live.append(plan.kernel_time())
         torch.cuda.synchronize(dev)
         t_wall = time.perf_counter() - t_wall
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
+    launches = launches_per_step * args.steps
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
+        n = torch.tensor([launches], dtype=torch.int64, device=dev)
+        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+        launches = int(n.item())
         dist.barrier()
     ms_per_step = total_ms / args.steps
     total_samples = cfg.samples()
@@ -255,17 +365,24 @@ def run_ours(args) -> None:
 
     # ---- the one collective (N > 1): digest rows of every degree shard gathered on rank 0
     gather = None
+    full_dig = dig_dev
     if world > 1:
         from paper_1207_5558_b200.parallel import gather_digests
 
         g0 = torch.cuda.Event(enable_timing=True)
         g1 = torch.cuda.Event(enable_timing=True)
         g0.record()
-        full = gather_digests(dig_dev, l0, l1, cfg.L_g)
+        full_dig = gather_digests(dig_dev, l0, l1, cfg.L_g)
         g1.record()
         torch.cuda.synchronize(dev)
         gather = {"ms": g0.elapsed_time(g1), "rows": int((cfg.L_g + 1) ** 2),
-                  "complete": bool(rank != 0 or not torch.isnan(full).any().item())}
+                  "backend": "nccl all_gather of padded row blocks"}
+    rt_err = None
+    complete = None
+    if rank == 0:
+        d = full_dig.cpu().numpy()
+        complete = bool(not np.isnan(d).any())
+        rt_err = roundtrip_error(d, f_np, h_np, cfg)
 
     # ---- e2e: C ABI with host buffers (pinned), H2D of f, h and D2H of digests inside
     f_pin = torch.from_numpy(f_np.view(np.float64).copy()).pin_memory()
@@ -287,15 +404,15 @@ def run_ours(args) -> None:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    dig_rows = plan.emitted_count
+    r0, r1 = l0 * l0, l1 * l1
     e2e = {"value": total_samples / e2e_s, "unit": "samples/s",
            "h2d_bytes_per_step": int(f_np.nbytes + h_np.nbytes),
-           "d2h_bytes_per_step": int(dig_pin.numel() * 8),
-           "digest_rows_per_rank": dig_rows,
-           "how": "slsht_cuda_forward_device(host f, h -> host digests), wall clock, mean of steps"}
+           "d2h_bytes_per_step": int((r1 - r0) * S.DIGEST_WIDTH * 8),
+           "how": ("slsht_cuda_forward_device(host f, h -> host digests of the rank's degree "
+                   "shard), wall clock, mean of steps, max over ranks")}
 
-    # ---- per-stage device times: two profiled steps after the timed ones (events between
-    # the kernels on the engine stream); the roofline's kernel time comes from the timed steps
+    # ---- per-stage device times: two profiled steps after the timed ones (events between the
+    # kernels on the engine stream); the roofline's kernel time comes from the timed steps
     # themselves when the plan is one chunk
     plan.set_profiling(True)
     prof = []
@@ -305,79 +422,91 @@ def run_ours(args) -> None:
         prof.append(plan.stage_times())
     plan.set_profiling(False)
     stage_ms = [statistics.mean(x) for x in zip(*prof)]
-    live = [x for x in live_stages if x is not None]
-    if single_chunk and len(live) == args.steps:
-        kernel_ms = statistics.mean(live)
-        stage_src = "CUDA events around the kernel on the engine stream in every timed step (mean)"
-    else:
-        kernel_ms = stage_ms[3]
-        stage_src = "CUDA events on the engine stream, two profiled steps after the timed ones"
     names = ["setup", "legendre", "modgemm", "couple", "digest", "qfft"]
     stages = dict(zip(names, stage_ms))
     two_pass = len(stage_ms) > 5 and stage_ms[5] > 0
-    couple_ms = kernel_ms
+    live = [x for x in live if x is not None]
     peaks = load_peaks()
-    alg_bytes = my_samples * 16.0  # one complex128 store per emitted sample
-    achieved = alg_bytes / (couple_ms / 1e3) / 1e9
+    alg_bytes = my_samples * 16.0  # one complex128 store per emitted sample (SURVEY §8(d))
+    fp64 = total_samples * cfg.flops_per_sample() / (ms_per_step / 1e3) / 1e12
+    fp64_view = {"canonical_flops_per_sample": cfg.flops_per_sample(),
+                 "achieved_tflops_canonical": fp64, "peak_tflops": P_FP64_TFLOPS,
+                 "frac": fp64 / P_FP64_TFLOPS, "peak_source": FP64_SOURCE}
+    step_roof = min(peaks["hbm_gbs"] * 1e9 / 16.0, P_FP64_TFLOPS * 1e12 / cfg.flops_per_sample())
     traffic = None
     tfile = ROOT / "profiles" / f"traffic_config{args.config}.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
-    fp64_view = {
-        "canonical_flops_per_sample": cfg.flops_per_sample(),
-        "achieved_tflops_canonical": total_samples * cfg.flops_per_sample() / (ms_per_step / 1e3) / 1e12,
-        "peak_tflops": P_FP64_TFLOPS,
-        "frac": total_samples * cfg.flops_per_sample() / (ms_per_step / 1e3) / 1e12 / P_FP64_TFLOPS,
-        "peak_source": "measured DMMA m8n8k4 peak (profiles/fp64_peak.txt)",
-    }
-    step_roof = min(peaks["hbm_gbs"] * 1e9 / 16.0, P_FP64_TFLOPS * 1e12 / cfg.flops_per_sample())
     if two_pass:
-        # two-pass coupling (n = 65, 129): k_tgemm (FP64 DMMA GEMM, T to HBM) and k_qfft (alpha
-        # FFT, HBM-bound: T read + volumes written); the dominant one is the roofline kernel
+        # two-pass coupling (n = 49, 65, 129): k_tgemm (FP64 DMMA GEMM, T to HBM) and k_qfft
+        # (alpha FFT + epilogue); the roofline kernel is the longer of the two. Algorithmic
+        # bytes of k_qfft are the emitted samples only (16 B each, §8(d)); the T re-read is
+        # overhead of this design and is shown separately.
         n, nb = 2 * cfg.L_h + 1, cfg.L_h + 1
         comps = plan.computed_count
-        gemm_flops = 8.0 * comps * (cfg.L_h + 1) ** 2 * n * nb  # complex MACs x 8
+        gemm_flops = 8.0 * comps * (cfg.L_h + 1) ** 2 * n * nb  # complex MACs x 8 (canonical)
         tg_ms, qf_ms = stage_ms[3], stage_ms[5]
-        qf_bytes = 16.0 * comps * n * n * nb + alg_bytes  # T read + emitted samples written
+        t_bytes = 16.0 * comps * n * n * nb
         tg = {"bound": "tensor", "kernel": "k_tgemm (coupling GEMM on the FP64 tensor cores)",
               "achieved": gemm_flops / (tg_ms / 1e3) / 1e12, "peak": P_FP64_TFLOPS,
               "unit": "TFLOP/s", "frac": gemm_flops / (tg_ms / 1e3) / 1e12 / P_FP64_TFLOPS,
-              "traffic": None, "peak_source": "measured DMMA m8n8k4 peak (profiles/fp64_peak.txt)",
+              "traffic": None, "peak_source": FP64_SOURCE,
+              "flop_model": "8 FLOP per complex MAC (the DMMA Gauss product issues 6)",
               "algorithmic_flops_per_step": gemm_flops, "kernel_ms_per_step": tg_ms}
         qf = {"bound": "hbm", "kernel": "k_qfft (alpha FFT + store/digest epilogue)",
-              "achieved": qf_bytes / (qf_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-              "frac": qf_bytes / (qf_ms / 1e3) / 1e9 / peaks["hbm_gbs"], "traffic": None,
-              "peak_source": peaks["source"] + " (MEASURED_PEAKS.json hbm_gbs)",
-              "algorithmic_bytes_per_step": qf_bytes, "kernel_ms_per_step": qf_ms}
+              "achieved": alg_bytes / (qf_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
+              "unit": "GB/s", "frac": alg_bytes / (qf_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+              "traffic": traffic, "peak_source": peaks["source"],
+              "algorithmic_bytes_per_step": alg_bytes, "kernel_ms_per_step": qf_ms,
+              "t_reread_bytes_per_step": t_bytes,
+              "moved_gbs_incl_t_reread": (alg_bytes + t_bytes) / (qf_ms / 1e3) / 1e9}
         main, other = (tg, qf) if tg_ms >= qf_ms else (qf, tg)
         roofline = dict(main)
         roofline.update({
             "kernel_ms_source": "CUDA events on the engine stream, two profiled steps after the timed ones",
             "kernel_share_of_step": main["kernel_ms_per_step"] / sum(stage_ms),
             "second_kernel": other, "fp64_view": fp64_view,
-            "step_roofline_samples_per_s": step_roof})
+            "step_roofline_samples_per_s": step_roof,
+            "step_frac_of_roofline": value / step_roof})
     else:
-        roofline = None
-    roofline = roofline or {
-        "bound": "hbm", "kernel": "k_couple (coupling DMMA + alpha FFT + store/digest epilogue)",
-        "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-        "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-        "peak_source": peaks["source"] + " (MEASURED_PEAKS.json hbm_gbs)",
-        "algorithmic_bytes_per_step": alg_bytes,
-        "kernel_ms_per_step": couple_ms,
-        "kernel_ms_source": stage_src,
-        "kernel_share_of_step": couple_ms / sum(stage_ms) if sum(stage_ms) > 0 else None,
-        "fp64_view": fp64_view,
-        "step_roofline_samples_per_s": step_roof,
-    }
+        if single_chunk and len(live) == args.steps:
+            couple_ms = statistics.mean(live)
+            src = "CUDA events around the kernel on the engine stream in every timed step (mean)"
+        else:
+            couple_ms = stage_ms[3]
+            src = "CUDA events on the engine stream, two profiled steps after the timed ones"
+        achieved = alg_bytes / (couple_ms / 1e3) / 1e9
+        roofline = {
+            "bound": "hbm", "kernel": "k_couple (coupling DMMA + alpha FFT + store/digest epilogue)",
+            "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+            "peak_source": peaks["source"], "algorithmic_bytes_per_step": alg_bytes,
+            "kernel_ms_per_step": couple_ms, "kernel_ms_source": src,
+            "kernel_share_of_step": couple_ms / sum(stage_ms) if sum(stage_ms) > 0 else None,
+            "fp64_view": fp64_view, "step_roofline_samples_per_s": step_roof,
+            "step_frac_of_roofline": value / step_roof,
+        }
+    steady_ms = max(ms_per_step - stages["setup"], 1e-9)
+    steady = {"value": total_samples / (steady_ms / 1e3), "unit": "samples/s",
+              "how": ("setup excluded: ms_per_step minus the setup stage on the engine stream "
+                      "(k_setup_main; the Delta -> W chain runs beside it on the auxiliary "
+                      "stream), profiled steps")}
 
+    host_sink = None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
+            host_sink = host_sink_sample(S, C, cfg, f_np, h_np, local)
+        except Exception as e:
+            host_sink = {"value": None, "error": f"{type(e).__name__}: {e}"}
+        try:
             threads = os.cpu_count() or 1
-            r = reference_sample(args.config, 2, 1, threads)
-            cpu = {"value": r["value"], "unit": "samples/s", "cores": r["cores"],
-                   "kind": "reference", "sample": r["sample"], "cpu": r["cpu"]}
+            rt = ReferenceTimer(args.config, threads)
+            meas, full = rt.run()
+            cpu = {"value": cfg.samples() / full, "unit": "samples/s", "cores": threads,
+                   "kind": "reference", "sample": rt.sample_text(1), "cpu": cpu_model(),
+                   "extrapolated": rt.ls is not None, "measured_s": meas,
+                   "full_run_s": full}
         except Exception as e:
             cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {type(e).__name__}: {e}"}
@@ -396,27 +525,23 @@ def run_ours(args) -> None:
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded BASELINE recipe; Slepian windows solved by the reference)",
-            "config": {
-                "workload": f"config{args.config}: forward_fast L_f={cfg.L_f} L_h={cfg.L_h} "
-                            f"{'real-mode' if cfg.real_mode else 'full-m'} ({cfg.description})",
-                "L_f": cfg.L_f, "L_h": cfg.L_h, "real_mode": cfg.real_mode,
-                "samples_per_step": total_samples,
-                "computed_components": cfg.computed(), "emitted_components": cfg.emitted(),
-                "output": ("materialized device distribution" if materialize else
-                           "device ring consumed by the fused digest epilogue"),
-                "l2": "256 MiB L2 flush between timed steps (outside the event pairs)",
-                "parallelism": f"l-shard x{world}",
-            },
+            "config": workload_config(cfg, world),
+            "output": ("materialized device distribution" if materialize else
+                       "device ring consumed by the fused digest epilogue"),
             "step_ms": {"min": min(step_ms), "max": max(step_ms),
                         "wall_ms_per_step": t_wall * 1e3 / args.steps},
             "stages_ms": stages,
             "e2e": e2e,
+            "steady_state": steady,
+            "host_sink": host_sink,
+            "roundtrip_err": rt_err,
+            "digests_complete": complete,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
             "gather": gather,
-            "gpu_launches": launches_per_step * args.steps,
-            "gpu_launches_per_step": launches_per_step,
+            "gpu_launches": launches,
+            "gpu_launches_per_step_per_rank": launches_per_step,
         }
         print(json.dumps(line))
     plan.close()
@@ -427,17 +552,19 @@ def run_ours(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ring-mb", type=int, default=24576)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args))
+    run_ours(args)
 
 
 if __name__ == "__main__":

@@ -60,15 +60,46 @@ typedef struct slsht_cuda_desc {
   int materialize;     /* 1: keep every emitted volume resident on the device at slot
                           coeff_index(l, m) (the materialized forward_fast, transform.cpp:297-311);
                           0: stream volumes through a device ring consumed by the epilogue */
-  int reserved0;
-  long long ring_bytes; /* ring capacity for materialize == 0 (0: automatic) */
-  void* stream;        /* cudaStream_t to run on (NULL: the plan creates its own) */
+  int n_devices;       /* 0 or 1: one device (`device`); > 1: a multi-GPU plan over devices[] */
+  long long ring_bytes; /* ring capacity for materialize == 0 (0: automatic), per device */
+  void* stream;        /* cudaStream_t to run on (NULL: the plan creates its own; ignored by
+                          multi-GPU plans, which own one stream per device) */
+  const int* devices;  /* n_devices > 1: CUDA ordinals, one degree shard each (an ordinal may
+                          repeat: several shards on one device) */
 } slsht_cuda_desc;
+
+/* Multi-GPU plans (the reference's forward_fast owns its whole parallel
+ * schedule, transform.cpp:260-294). The degree range [l_begin, l_end) is split into n_devices
+ * contiguous shards balanced by computed components (c(l) = 2l+1, or l+1 in real mode), shard k
+ * on devices[k]; the shards share nothing while computing. The only exchange is the final
+ * gather: each shard's digest rows [l0^2, l1^2) are copied (cudaMemcpyDefault: peer-to-peer
+ * over NVLink for a device destination) into the caller's table; rows are copied, never
+ * reduced, so every result is bitwise the one-device result. Host-sink calls of the shards are
+ * serialized under one mutex, as the reference's worker pool does (transform.cpp:282-284). */
+
+/* The shard rule of multi-GPU plans (host only, no device needed): bounds[0..parts] of the
+ * degree range [l_begin, l_end) for `parts` shards. Returns 0, or SLSHT_ERR_VALIDATION. */
+int slsht_cuda_shard_bounds(int l_begin, int l_end, int real_mode, int parts, int* bounds);
 
 /* Host sink, called once per emitted component with a pointer valid only during the call
  * (the So3Volume& contract of ComponentSink, transform.hpp:142-143, transform.cpp:279-284).
  * Calls are serialized on the calling thread. */
 typedef void (*slsht_host_sink)(int l, int m, const double* volume, void* user);
+
+/* Host copy sink: the copy the materializing forward_fast performs for every component
+ * (transform.cpp:297-311, `components[coeff_index(l, m)] = volume`). Pass it as the sink of
+ * slsht_cuda_forward with user = a slsht_copy_target: the volume of (l, m) is copied to
+ * base + (coeff_index(l, m) - first_index) * volume_elems complex when that row lies in
+ * [first_index, first_index + count); other rows are counted in `dropped`. */
+typedef struct slsht_copy_target {
+  double* base;
+  long long first_index;
+  long long count;
+  long long volume_elems;
+  long long delivered; /* volumes copied */
+  long long dropped;   /* volumes outside the target range */
+} slsht_copy_target;
+void slsht_cuda_copy_sink(int l, int m, const double* volume, void* target);
 
 int slsht_cuda_plan_create(const slsht_cuda_desc* desc, slsht_cuda_plan** plan);
 void slsht_cuda_plan_destroy(slsht_cuda_plan* plan);

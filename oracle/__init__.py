@@ -192,6 +192,9 @@ class Reference(_Lib):
         L.ref_random_coeffs.argtypes = [C.c_int, C.c_uint64, C.c_int, _dp]
         L.ref_components.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_int, C.POINTER(C.c_int),
                                      C.POINTER(C.c_int), _dp]
+        L.ref_components_mt.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_int, C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int), C.c_int, _dp]
+        L.ref_setup_seconds.argtypes = [C.c_int, _dp, C.c_int, C.c_int, _dp, C.c_int, _dp]
         L.ref_rotate_coeffs.argtypes = [C.c_int, _dp, C.c_double, C.c_double, C.c_double, _dp]
         L.ref_forward_direct.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_int, C.c_int, _dp]
 
@@ -289,6 +292,28 @@ class Reference(_Lib):
                                            _ptr(np.ascontiguousarray(h, dtype=np.complex128)),
                                            len(lm), ls, ms, _ptr(out)))
         return {k: out[i] for i, k in enumerate(lm)}
+
+    def components_mt(self, f, L_f, h, L_h, lm, threads: int = 0) -> np.ndarray:
+        """Volumes [len(lm), n, L_h+1, n] of the listed (l, m) through the component chain on
+        `threads` host threads (0: all cores)."""
+        lm = list(lm)
+        ls = (C.c_int * len(lm))(*[l for l, _ in lm])
+        ms = (C.c_int * len(lm))(*[m for _, m in lm])
+        out = np.zeros((len(lm),) + volume_shape(L_h), dtype=np.complex128)
+        nt = threads or os.cpu_count() or 1
+        self.check(self.lib.ref_components_mt(
+            L_f, _ptr(np.ascontiguousarray(f, dtype=np.complex128)), L_h,
+            _ptr(np.ascontiguousarray(h, dtype=np.complex128)), len(lm), ls, ms, nt, _ptr(out)))
+        return out
+
+    def setup_seconds(self, f, L_f, f_real, h, L_h, h_real) -> float:
+        """Wall time of forward_fast's per-call setup (ModulatedSht + DeltaTables +
+        So3Evaluator, transform.cpp:256-258)."""
+        secs = np.zeros(1)
+        self.check(self.lib.ref_setup_seconds(
+            L_f, _ptr(np.ascontiguousarray(f, dtype=np.complex128)), int(f_real), L_h,
+            _ptr(np.ascontiguousarray(h, dtype=np.complex128)), int(h_real), _ptr(secs)))
+        return float(secs[0])
 
     def forward_direct(self, f, L_f, h, L_h, lmax=-1, threads=0) -> np.ndarray:
         """forward_direct (transform.cpp:313-388): [coeff_count(lmax), V] complex."""

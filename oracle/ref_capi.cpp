@@ -10,12 +10,15 @@
 // slsht::NumericError and 1 for anything else, mirroring the reference CLI's exit codes
 // (proj/src/cli.cpp:31-45).
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <chrono>
 #include <cmath>
 #include <complex>
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "slsht/errors.hpp"
@@ -252,6 +255,69 @@ int ref_components(int L_f, const double* f, int L_h, const double* h, int count
       ev.evaluate(c, es, vol);
       std::memcpy(out + 2 * V * static_cast<std::size_t>(i), vol.values.data(), sizeof(double) * 2 * V);
     }
+  });
+}
+
+// The same chain on `threads` worker threads (each with its own scratch, as forward_fast's pool
+// does, transform.cpp:263-294); the shared ModulatedSht / DeltaTables / So3Evaluator are const.
+// Components are independent, so every volume is bitwise the single-threaded one.
+int ref_components_mt(int L_f, const double* f, int L_h, const double* h, int count, const int* l,
+                      const int* m, int threads, double* out) {
+  return guarded([&] {
+    const slsht::SphCoeffs fc = make_coeffs(L_f, f, 0);
+    const slsht::SphCoeffs hc = make_coeffs(L_h, h, 0);
+    const slsht::ModulatedSht ctx(fc, L_h);
+    const slsht::DeltaTables delta(L_h);
+    const slsht::So3Evaluator ev(L_h);
+    const std::size_t V = static_cast<std::size_t>(2 * L_h + 1) * (2 * L_h + 1) * (L_h + 1);
+    std::atomic<int> next{0};
+    std::string first_error;
+    std::mutex err_mutex;
+    auto worker = [&] {
+      try {
+        slsht::ModulatedSht::Scratch scratch;
+        slsht::So3Evaluator::Scratch es;
+        slsht::ModulatedCoeffs mod;
+        slsht::CTensor c;
+        slsht::So3Volume vol;
+        for (;;) {
+          const int i = next.fetch_add(1);
+          if (i >= count) break;
+          ctx.compute(l[i], m[i], scratch, mod);
+          slsht::build_c_tensor(mod, hc, delta, c);
+          ev.evaluate(c, es, vol);
+          std::memcpy(out + 2 * V * static_cast<std::size_t>(i), vol.values.data(),
+                      sizeof(double) * 2 * V);
+        }
+      } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> lock(err_mutex);
+        if (first_error.empty()) first_error = e.what();
+        next.store(count);
+      }
+    };
+    const int nt = std::max(1, std::min(threads, count));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+    if (!first_error.empty()) throw slsht::ValidationError(first_error);
+  });
+}
+
+// The per-call setup of forward_fast (transform.cpp:256-258): ModulatedSht (serial: the I table
+// and the window Legendre table), DeltaTables and So3Evaluator, timed with steady_clock. The
+// CPU-baseline extrapolation of SURVEY.md §8(d) subtracts it from a sampled run.
+int ref_setup_seconds(int L_f, const double* f, int f_real, int L_h, const double* h, int h_real,
+                      double* seconds) {
+  return guarded([&] {
+    const slsht::SphCoeffs fc = make_coeffs(L_f, f, f_real);
+    const slsht::SphCoeffs hc = make_coeffs(L_h, h, h_real);
+    const auto t0 = std::chrono::steady_clock::now();
+    const slsht::ModulatedSht ctx(fc, L_h);
+    const slsht::DeltaTables delta(L_h);
+    const slsht::So3Evaluator ev(L_h);
+    const auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
   });
 }
 

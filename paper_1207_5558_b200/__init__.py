@@ -7,11 +7,11 @@ from ._lib import DIGEST_WIDTH, LIB_PATH, load
 from .transform import (DeviceError, ForwardOptions, NumericError, Plan, SlshtDistribution,
                         SphCoeffs, ValidationError, coeff_count, coeff_index, delta_tables,
                         eigenfunction_window, forward_direct, forward_fast, modulated_sht,
-                        volume_shape)
+                        shard_bounds, volume_shape)
 
 __all__ = [
     "DIGEST_WIDTH", "LIB_PATH", "load", "DeviceError", "ForwardOptions", "NumericError", "Plan",
     "SlshtDistribution", "SphCoeffs", "ValidationError", "coeff_count", "coeff_index",
     "delta_tables", "eigenfunction_window", "forward_direct", "forward_fast", "modulated_sht",
-    "volume_shape",
+    "shard_bounds", "volume_shape",
 ]

@@ -41,6 +41,8 @@ EXPORTS = [
     "slsht_cuda_inverse",
     "slsht_cuda_eigenfunction_window",
     "slsht_cuda_forward_direct",
+    "slsht_cuda_copy_sink",
+    "slsht_cuda_shard_bounds",
 ]
 
 
@@ -55,9 +57,21 @@ class slsht_cuda_desc(C.Structure):
         ("l_begin", C.c_int),
         ("l_end", C.c_int),
         ("materialize", C.c_int),
-        ("reserved0", C.c_int),
+        ("n_devices", C.c_int),
         ("ring_bytes", C.c_longlong),
         ("stream", C.c_void_p),
+        ("devices", C.POINTER(C.c_int)),
+    ]
+
+
+class slsht_copy_target(C.Structure):
+    _fields_ = [
+        ("base", C.c_void_p),
+        ("first_index", C.c_longlong),
+        ("count", C.c_longlong),
+        ("volume_elems", C.c_longlong),
+        ("delivered", C.c_longlong),
+        ("dropped", C.c_longlong),
     ]
 
 
@@ -84,7 +98,7 @@ def load() -> C.CDLL:
     lib.slsht_cuda_plan_destroy.restype = None
     lib.slsht_cuda_last_error.argtypes = [C.c_void_p]
     lib.slsht_cuda_last_error.restype = C.c_char_p
-    lib.slsht_cuda_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, SINK, C.c_void_p]
+    lib.slsht_cuda_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.slsht_cuda_forward.restype = C.c_int
     lib.slsht_cuda_forward_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                               C.c_void_p, C.c_int, C.c_int]
@@ -119,5 +133,7 @@ def load() -> C.CDLL:
     lib.slsht_cuda_inverse.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
                                        C.c_double, C.c_int, C.c_void_p]
     lib.slsht_cuda_inverse.restype = C.c_int
+    lib.slsht_cuda_shard_bounds.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip]
+    lib.slsht_cuda_shard_bounds.restype = C.c_int
     _lib = lib
     return lib

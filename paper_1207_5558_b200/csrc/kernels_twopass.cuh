@@ -36,6 +36,8 @@ struct TgParams {
   double2* T;            // [comp][n][ncolp]
   const short* qend;     // per k-step: T row (q mod n) completed by it, or -1
   int count, KP, ncolp, n;
+  int col_fast;          // 1: blockIdx.x = column tile (W L2-resident, U block read once)
+  int t_stream;          // 1: T stored with the evict-first (.cs) hint
 };
 
 __host__ __device__ constexpr int tgemm_threads(int BN, int WNF, int BM = TG_BM) {
@@ -48,6 +50,12 @@ __host__ __device__ constexpr size_t tgemm_smem_bytes(int KP, int BN, int NST, i
 // 256-bit global store (sm_100): two consecutive complex values
 __device__ __forceinline__ void st_global_v4(double2* p, double a, double b, double c, double d) {
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+// the same with the streaming (evict-first) hint
+__device__ __forceinline__ void st_global_cs_v4(double2* p, double a, double b, double c, double d) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d)
                : "memory");
 }
 
@@ -64,9 +72,12 @@ __global__ void __launch_bounds__(tgemm_threads(BN, WNF, BM), MINB) k_tgemm(cons
   double2* Bs = As + TG_NST * BM * TG_ASTR;
   short* qend_s = reinterpret_cast<short*>(Bs + TG_NST * TG_KS * TG_BSTR);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // grid x = component block: the CTAs in flight share a few W column tiles (read from HBM
-  // once per chunk) while the chunk's U stays L2-resident
-  const int comp0 = blockIdx.x * BM, col0 = blockIdx.y * BN;
+  // raster (host-chosen, TgParams::col_fast): with a large W (config 5: 0.6 GB) grid x is the
+  // component block, so the CTAs in flight share a few W column tiles; with an L2-resident W
+  // (configs 3-4: <= 40 MB) grid x is the column tile, so the CTAs in flight share one U block
+  // and every U byte is read from HBM once per chunk
+  const int bx = P.col_fast ? blockIdx.y : blockIdx.x, by = P.col_fast ? blockIdx.x : blockIdx.y;
+  const int comp0 = bx * BM, col0 = by * BN;
   const int nks = P.KP / 4, nst = (P.KP + TG_KS - 1) / TG_KS;
   for (int i = tid; i < nks; i += TG_THREADS) qend_s[i] = P.qend[i];
 
@@ -156,9 +167,16 @@ __global__ void __launch_bounds__(tgemm_threads(BN, WNF, BM), MINB) k_tgemm(cons
           if (comp < P.count) {
             double2* dst = P.T + ((size_t)comp * P.n + row) * P.ncolp + scol;
 #pragma unroll
-            for (int ni = 0; ni < WNF; ++ni)  // 32 B per lane: 4 lanes write one whole 128-B line
-              st_global_v4(dst + ni * 8, c1[mi][ni][0] - c3[mi][ni][0], c1[mi][ni][0] + c2[mi][ni][0],
-                           c1[mi][ni][1] - c3[mi][ni][1], c1[mi][ni][1] + c2[mi][ni][1]);
+            for (int ni = 0; ni < WNF; ++ni) {  // 32 B per lane: 4 lanes write one whole 128-B line
+              if (P.t_stream)
+                st_global_cs_v4(dst + ni * 8, c1[mi][ni][0] - c3[mi][ni][0],
+                                c1[mi][ni][0] + c2[mi][ni][0], c1[mi][ni][1] - c3[mi][ni][1],
+                                c1[mi][ni][1] + c2[mi][ni][1]);
+              else
+                st_global_v4(dst + ni * 8, c1[mi][ni][0] - c3[mi][ni][0],
+                             c1[mi][ni][0] + c2[mi][ni][0], c1[mi][ni][1] - c3[mi][ni][1],
+                             c1[mi][ni][1] + c2[mi][ni][1]);
+            }
           }
         }
       }

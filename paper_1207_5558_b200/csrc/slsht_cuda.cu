@@ -9,7 +9,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kernels_chunk.cuh"
@@ -124,6 +126,8 @@ struct slsht_cuda_plan {
   int tp_bn = 64;          //   k_tgemm column tile (32 in the overlapped schedule)
   int tp_gv = 3;           //   k_tgemm variant (tgemm_variant)
   bool tp_overlap = false; //   k_qfft + digest of chunk i on fft_stream under k_tgemm of i+1
+  bool tp_col_fast = false; //  k_tgemm raster: column tiles fastest (W L2-resident)
+  bool tp_t_stream = false; //  k_tgemm: T stores with the evict-first hint
   size_t tp_t_elems = 0;   //   one T buffer (two in the overlapped schedule)
   cudaStream_t fft_stream = nullptr;
   cudaEvent_t ev_tg[2] = {}, ev_fft[2] = {};
@@ -186,12 +190,22 @@ struct slsht_cuda_plan {
   // inside the CUDA graph), read lazily by slsht_cuda_kernel_time
   cudaEvent_t ev_lazy[2] = {};
   bool lazy_valid = false;
+  // multi-GPU plan (desc.n_devices > 1): one single-device plan per degree shard; this object
+  // then only holds the group-level sizes and dispatches
+  std::vector<slsht_cuda_plan*> parts;
+  std::vector<int> part_bounds;  // shard k = degrees [part_bounds[k], part_bounds[k+1])
+  bool group() const { return !parts.empty(); }
 };
 
 namespace {
 
 void free_plan(slsht_cuda_plan* p) {
   if (!p) return;
+  for (slsht_cuda_plan* q : p->parts) {
+    cudaSetDevice(q->desc.device);
+    free_plan(q);
+  }
+  p->parts.clear();
   cudaFree(p->d_f);
   cudaFree(p->d_T);
   cudaFree(p->d_qend);
@@ -572,6 +586,11 @@ void build_plan(slsht_cuda_plan* p) {
     urb[p->n] = rows_pad;
     rows_pad = (rows_pad + TG_KS - 1) / TG_KS * TG_KS;  // whole GEMM stages (zero rows)
     p->tp_KP = rows_pad;
+    // k_tgemm raster: column tiles fastest when W (KP x ncolp complex) stays L2-resident, so a
+    // chunk's U is read from HBM once (SLSHT_CUDA_TG_RASTER=0/1 forces either order)
+    p->tp_col_fast = (size_t)p->tp_KP * p->tp_ncolp * 16 <= (48u << 20);
+    if (const char* e = std::getenv("SLSHT_CUDA_TG_RASTER")) p->tp_col_fast = e[0] == '1';
+    if (const char* e = std::getenv("SLSHT_CUDA_TG_STREAM")) p->tp_t_stream = e[0] == '1';
     qend.assign(rows_pad / 4, (short)-1);
     for (int jq = 0; jq < p->n; ++jq) {
       for (int c = qoff[jq]; c < qoff[jq + 1]; ++c) {
@@ -1022,7 +1041,10 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     tg.ncolp = p->tp_ncolp;
     tg.n = p->n;
     const int tbm = tgemm_variant(p->tp_gv).bm;
-    const dim3 tgrid((ch.count + tbm - 1) / tbm, p->tp_ncolp / p->tp_bn);
+    tg.col_fast = p->tp_col_fast ? 1 : 0;
+    tg.t_stream = p->tp_t_stream ? 1 : 0;
+    const int nbm = (ch.count + tbm - 1) / tbm, nbn = p->tp_ncolp / p->tp_bn;
+    const dim3 tgrid(tg.col_fast ? nbn : nbm, tg.col_fast ? nbm : nbn);
     if (p->tp_gv == 2) {
       // the GEMM of chunk i+1 is dispatched ahead of the FFT CTAs of chunk i (one GEMM CTA per
       // SM, one FFT CTA beside it)
@@ -1107,7 +1129,8 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
 }
 
 void load_inputs(slsht_cuda_plan* p, const double* f, const double* h, bool on_device) {
-  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  // device inputs may live on another GPU of a multi-GPU plan: UVA resolves the direction
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDefault : cudaMemcpyHostToDevice;
   CK(cudaMemcpyAsync(p->d_f, f, sizeof(double) * 2 * coeff_count(p->L_f), kind, p->stream));
   CK(cudaMemcpyAsync(p->d_h, h, sizeof(double) * 2 * coeff_count(p->L_h), kind, p->stream));
 }
@@ -1117,8 +1140,10 @@ void load_inputs(slsht_cuda_plan* p, const double* f, const double* h, bool on_d
 void copy_digests(slsht_cuda_plan* p, double* digests, bool on_device) {
   const size_t r0 = (size_t)p->l_begin * p->l_begin, r1 = (size_t)p->l_end * p->l_end;
   if (r1 <= r0) return;
+  if (digests == p->d_digest) return;  // already in place
+  // the gather of a multi-GPU plan: a device destination may be a peer GPU (NVLink P2P)
   CK(cudaMemcpyAsync(digests + 8 * r0, p->d_digest + 8 * r0, (r1 - r0) * 8 * sizeof(double),
-                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, p->stream));
+                     on_device ? cudaMemcpyDefault : cudaMemcpyDeviceToHost, p->stream));
 }
 
 void check_numeric(slsht_cuda_plan* p) {
@@ -1150,6 +1175,120 @@ int guarded(slsht_cuda_plan* p, F&& fn) {
   }
 }
 
+// Degree shards of a multi-GPU plan, balanced by computed components: c(l) = 2l+1 (full-m) or
+// l+1 (real mode); bound k is the first degree whose cumulative count reaches k/parts of the
+// total (the same rule as paper_1207_5558_b200.configs.shard_degrees).
+std::vector<int> shard_bounds(int l_begin, int l_end, bool real_mode, int parts) {
+  std::vector<double> cum(1, 0.0);
+  for (int l = l_begin; l < l_end; ++l) cum.push_back(cum.back() + (real_mode ? l + 1.0 : 2.0 * l + 1.0));
+  const double total = cum.back();
+  std::vector<int> b(parts + 1);
+  b[0] = l_begin;
+  for (int k = 1; k < parts; ++k) {
+    const double x = total * k / parts;
+    const int i = (int)(std::lower_bound(cum.begin(), cum.end(), x) - cum.begin());
+    b[k] = std::min(std::max(l_begin + i, l_begin), l_end);
+  }
+  b[parts] = l_end;
+  for (int k = 1; k <= parts; ++k) b[k] = std::max(b[k], b[k - 1]);
+  return b;
+}
+
+// A multi-GPU plan: one single-device plan per shard.
+void build_group(slsht_cuda_plan* p) {
+  const slsht_cuda_desc& d = p->desc;
+  if (!d.devices) throw Status{SLSHT_ERR_VALIDATION, "n_devices > 1 needs a device list"};
+  if (d.L_f < 0 || d.L_h < 0) throw Status{SLSHT_ERR_VALIDATION, "band limit must be non-negative"};
+  p->L_f = d.L_f;
+  p->L_h = d.L_h;
+  p->L_g = d.L_f + d.L_h;
+  p->lmax = d.lmax < 0 ? p->L_g : d.lmax;
+  if (p->lmax > p->L_g)
+    throw Status{SLSHT_ERR_VALIDATION, "fast engine computes components up to L_f + L_h only"};
+  p->l_begin = std::max(0, d.l_begin);
+  p->l_end = d.l_end < 0 ? p->lmax + 1 : std::min(d.l_end, p->lmax + 1);
+  if (p->l_begin > p->l_end) throw Status{SLSHT_ERR_VALIDATION, "empty or inverted degree range"};
+  p->real_mode = d.real_mode ? 1 : 0;
+  p->emit_neg = d.emit_negative_m ? 1 : 0;
+  p->mirror = p->real_mode && p->emit_neg;
+  p->materialize = d.materialize ? 1 : 0;
+  p->n = 2 * d.L_h + 1;
+  p->nb = d.L_h + 1;
+  p->vol = (long long)p->n * p->n * p->nb;
+  p->part_bounds = shard_bounds(p->l_begin, p->l_end, p->real_mode, d.n_devices);
+  for (int k = 0; k < d.n_devices; ++k) {
+    slsht_cuda_desc pd = d;
+    pd.n_devices = 0;
+    pd.devices = nullptr;
+    pd.device = d.devices[k];
+    pd.stream = nullptr;
+    pd.l_begin = p->part_bounds[k];
+    pd.l_end = p->part_bounds[k + 1];
+    slsht_cuda_plan* q = new slsht_cuda_plan();
+    q->desc = pd;
+    p->parts.push_back(q);  // freed with the group on failure
+    build_plan(q);
+    p->emitted += q->emitted;
+    p->launches = 0;
+  }
+  p->desc.device = d.devices[0];
+  // direct NVLink P2P for the gather (the copies also work without it, staged by the driver)
+  for (int a = 0; a < d.n_devices; ++a)
+    for (int b = 0; b < d.n_devices; ++b) {
+      int ok = 0;
+      if (d.devices[a] == d.devices[b] ||
+          cudaDeviceCanAccessPeer(&ok, d.devices[a], d.devices[b]) != cudaSuccess || !ok)
+        continue;
+      cudaSetDevice(d.devices[a]);
+      if (cudaDeviceEnablePeerAccess(d.devices[b], 0) != cudaSuccess) cudaGetLastError();
+    }
+  CK(cudaSetDevice(p->desc.device));
+}
+
+long long group_computed(const slsht_cuda_plan* p) {
+  long long c = 0;
+  for (const slsht_cuda_plan* q : p->parts) c += (long long)q->comps.size();
+  return c;
+}
+
+void run_forward_device(slsht_cuda_plan* p, const double* f, const double* h,
+                        int inputs_on_device, double* digests, int digests_on_device,
+                        int synchronize);
+
+// Group forward_device: every shard is enqueued on its own device and stream, then each copies
+// its digest rows into the caller's table (the final gather); the call returns after all
+// shards finished.
+void run_group_device(slsht_cuda_plan* p, const double* f, const double* h, int inputs_on_device,
+                      double* digests, int digests_on_device) {
+  p->launches = 0;
+  for (slsht_cuda_plan* q : p->parts) {
+    CK(cudaSetDevice(q->desc.device));
+    run_forward_device(q, f, h, inputs_on_device, digests, digests_on_device, 0);
+  }
+  for (slsht_cuda_plan* q : p->parts) {
+    CK(cudaSetDevice(q->desc.device));
+    check_numeric(q);  // synchronizes the shard's stream
+    p->launches += q->launches;
+  }
+  CK(cudaSetDevice(p->desc.device));
+}
+
+struct LockedSink {
+  slsht_host_sink sink;
+  void* user;
+  std::mutex* mu;
+};
+void locked_sink(int l, int m, const double* vol, void* u) {
+  LockedSink* s = static_cast<LockedSink*>(u);
+  std::lock_guard<std::mutex> lock(*s->mu);
+  s->sink(l, m, vol, s->user);
+}
+
+void run_forward_sink(slsht_cuda_plan* p, const double* f, const double* h, slsht_host_sink sink,
+                      void* user);
+void run_capture(slsht_cuda_plan* p, const double* f, const double* h, double* digests, int count,
+                 const int* l, const int* m, const int* slot, double* volumes);
+
 }  // namespace
 
 extern "C" {
@@ -1164,7 +1303,8 @@ int slsht_cuda_plan_create(const slsht_cuda_desc* desc, slsht_cuda_plan** out) {
   p->desc = *desc;
   int rc = SLSHT_OK;
   try {
-    build_plan(p);
+    if (desc->n_devices > 1) build_group(p);
+    else build_plan(p);
   } catch (const Status& st) {
     g_create_error = st.msg;
     rc = st.code;
@@ -1191,6 +1331,10 @@ void slsht_cuda_plan_destroy(slsht_cuda_plan* p) {
 const char* slsht_cuda_last_error(const slsht_cuda_plan* p) {
   return p ? p->last_error.c_str() : g_create_error.c_str();
 }
+
+}  // extern "C"
+
+namespace {
 
 void run_forward_device(slsht_cuda_plan* p, const double* f, const double* h,
                         int inputs_on_device, double* digests, int digests_on_device,
@@ -1241,20 +1385,9 @@ void run_forward_device(slsht_cuda_plan* p, const double* f, const double* h,
   }
 }
 
-int slsht_cuda_forward_device(slsht_cuda_plan* p, const double* f, const double* h,
-                              int inputs_on_device, double* digests, int digests_on_device,
-                              int synchronize) {
-  if (!p) return SLSHT_ERR_VALIDATION;
-  return guarded(p, [&] {
-    run_forward_device(p, f, h, inputs_on_device, digests, digests_on_device, synchronize);
-  });
-}
-
-int slsht_cuda_forward_capture(slsht_cuda_plan* p, const double* f, const double* h,
-                               double* digests, int count, const int* l, const int* m,
-                               double* volumes) {
-  if (!p) return SLSHT_ERR_VALIDATION;
-  return guarded(p, [&] {
+void run_capture(slsht_cuda_plan* p, const double* f, const double* h, double* digests, int count,
+                 const int* l, const int* m, const int* slot, double* volumes) {
+  {
     // locate every request: (chunk, slot) of the component or of its conjugate mirror
     struct Req {
       size_t chunk;
@@ -1292,18 +1425,18 @@ int slsht_cuda_forward_capture(slsht_cuda_plan* p, const double* f, const double
       join_fft(p);
       for (const Req& r : reqs)
         if (r.chunk == ci)
-          CK(cudaMemcpyAsync(volumes + 2 * (size_t)r.i * p->vol, p->d_out + (size_t)r.slot * p->vol,
-                             (size_t)p->vol * 16, cudaMemcpyDeviceToHost, p->stream));
+          CK(cudaMemcpyAsync(volumes + 2 * (size_t)(slot ? slot[r.i] : r.i) * p->vol,
+                             p->d_out + (size_t)r.slot * p->vol, (size_t)p->vol * 16,
+                             cudaMemcpyDeviceToHost, p->stream));
     }
     if (digests) copy_digests(p, digests, false);
     check_numeric(p);
-  });
+  }
 }
 
-int slsht_cuda_forward(slsht_cuda_plan* p, const double* f, const double* h, slsht_host_sink sink,
-                       void* user) {
-  if (!p) return SLSHT_ERR_VALIDATION;
-  return guarded(p, [&] {
+void run_forward_sink(slsht_cuda_plan* p, const double* f, const double* h, slsht_host_sink sink,
+                      void* user) {
+  {
     if (p->materialize)
       throw Status{SLSHT_ERR_VALIDATION, "host-sink forward needs a streaming (ring) plan"};
     p->launches = 0;
@@ -1357,15 +1490,108 @@ int slsht_cuda_forward(slsht_cuda_plan* p, const double* f, const double* h, sls
     if (nc >= 1) deliver(nc - 1);
     join_fft(p);
     CK(cudaStreamSynchronize(p->stream));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int slsht_cuda_forward_device(slsht_cuda_plan* p, const double* f, const double* h,
+                              int inputs_on_device, double* digests, int digests_on_device,
+                              int synchronize) {
+  if (!p) return SLSHT_ERR_VALIDATION;
+  return guarded(p, [&] {
+    if (p->group()) run_group_device(p, f, h, inputs_on_device, digests, digests_on_device);
+    else run_forward_device(p, f, h, inputs_on_device, digests, digests_on_device, synchronize);
   });
 }
 
+int slsht_cuda_forward_capture(slsht_cuda_plan* p, const double* f, const double* h,
+                               double* digests, int count, const int* l, const int* m,
+                               double* volumes) {
+  if (!p) return SLSHT_ERR_VALIDATION;
+  return guarded(p, [&] {
+    if (!p->group()) {
+      run_capture(p, f, h, digests, count, l, m, nullptr, volumes);
+      return;
+    }
+    // each request goes to the shard that owns its degree; volumes keep the caller's order
+    std::vector<int> owner(count, -1);
+    for (int i = 0; i < count; ++i)
+      for (size_t k = 0; k < p->parts.size(); ++k)
+        if (l[i] >= p->part_bounds[k] && l[i] < p->part_bounds[k + 1]) owner[i] = (int)k;
+    for (int i = 0; i < count; ++i)
+      if (owner[i] < 0) throw Status{SLSHT_ERR_VALIDATION, "requested component not produced by this plan"};
+    for (size_t k = 0; k < p->parts.size(); ++k) {
+      std::vector<int> ls, ms, slot;
+      for (int i = 0; i < count; ++i)
+        if (owner[i] == (int)k) {
+          ls.push_back(l[i]);
+          ms.push_back(m[i]);
+          slot.push_back(i);
+        }
+      slsht_cuda_plan* q = p->parts[k];
+      CK(cudaSetDevice(q->desc.device));
+      run_capture(q, f, h, digests, (int)ls.size(), ls.data(), ms.data(), slot.data(), volumes);
+    }
+    CK(cudaSetDevice(p->desc.device));
+  });
+}
+
+int slsht_cuda_forward(slsht_cuda_plan* p, const double* f, const double* h, slsht_host_sink sink,
+                       void* user) {
+  if (!p) return SLSHT_ERR_VALIDATION;
+  return guarded(p, [&] {
+    if (!p->group()) {
+      run_forward_sink(p, f, h, sink, user);
+      return;
+    }
+    // one host thread per shard; sink calls serialized under one mutex (transform.cpp:282-284)
+    std::mutex mu;
+    LockedSink ls{sink, user, &mu};
+    std::vector<std::thread> pool;
+    std::vector<Status> errors(p->parts.size(), Status{SLSHT_OK, ""});
+    for (size_t k = 0; k < p->parts.size(); ++k)
+      pool.emplace_back([&, k] {
+        slsht_cuda_plan* q = p->parts[k];
+        try {
+          CK(cudaSetDevice(q->desc.device));
+          run_forward_sink(q, f, h, locked_sink, &ls);
+        } catch (const Status& st) {
+          errors[k] = st;
+        } catch (const CudaError& e) {
+          errors[k] = Status{SLSHT_ERR_DEVICE, e.msg};
+        } catch (const std::exception& e) {
+          errors[k] = Status{SLSHT_ERR_DEVICE, e.what()};
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (const Status& st : errors)
+      if (st.code != SLSHT_OK) throw st;
+  });
+}
+
+void slsht_cuda_copy_sink(int l, int m, const double* volume, void* target) {
+  slsht_copy_target* t = static_cast<slsht_copy_target*>(target);
+  if (!t || !volume) return;
+  const long long row = (long long)coeff_index(l, m) - t->first_index;
+  if (row < 0 || row >= t->count || !t->base) {
+    ++t->dropped;
+    return;
+  }
+  std::memcpy(t->base + 2 * row * t->volume_elems, volume, sizeof(double) * 2 * t->volume_elems);
+  ++t->delivered;
+}
+
 const double* slsht_cuda_device_output(const slsht_cuda_plan* p) {
-  return (p && p->materialize) ? reinterpret_cast<const double*>(p->d_out) : nullptr;
+  // a multi-GPU plan has no single device buffer
+  return (p && p->materialize && !p->group()) ? reinterpret_cast<const double*>(p->d_out) : nullptr;
 }
 long long slsht_cuda_volume_elems(const slsht_cuda_plan* p) { return p ? p->vol : 0; }
 long long slsht_cuda_computed_count(const slsht_cuda_plan* p) {
-  return p ? (long long)p->comps.size() : 0;
+  if (!p) return 0;
+  return p->group() ? group_computed(p) : (long long)p->comps.size();
 }
 long long slsht_cuda_emitted_count(const slsht_cuda_plan* p) { return p ? p->emitted : 0; }
 void* slsht_cuda_stream(const slsht_cuda_plan* p) { return p ? (void*)p->stream : nullptr; }
@@ -1374,17 +1600,38 @@ long long slsht_cuda_launch_count(const slsht_cuda_plan* p) { return p ? p->laun
 int slsht_cuda_set_profiling(slsht_cuda_plan* p, int enable) {
   if (!p) return SLSHT_ERR_VALIDATION;
   p->profile = enable != 0;
+  for (slsht_cuda_plan* q : p->parts) q->profile = enable != 0;
   return SLSHT_OK;
 }
 
 int slsht_cuda_stage_times(const slsht_cuda_plan* p, double* out_ms, int n) {
   if (!p || !out_ms) return 0;
   const int k = std::min(n, (int)ST_COUNT);
-  for (int i = 0; i < k; ++i) out_ms[i] = p->stage_ms[i];
+  for (int i = 0; i < k; ++i) {
+    out_ms[i] = p->stage_ms[i];
+    for (const slsht_cuda_plan* q : p->parts) out_ms[i] = std::max(out_ms[i], q->stage_ms[i]);
+  }
   return k;
 }
 
+int slsht_cuda_shard_bounds(int l_begin, int l_end, int real_mode, int parts, int* bounds) {
+  if (parts < 1 || !bounds || l_begin < 0 || l_end < l_begin) return SLSHT_ERR_VALIDATION;
+  const std::vector<int> b = shard_bounds(l_begin, l_end, real_mode != 0, parts);
+  std::copy(b.begin(), b.end(), bounds);
+  return SLSHT_OK;
+}
+
 int slsht_cuda_kernel_time(const slsht_cuda_plan* p, double* ms_out) {
+  if (p && ms_out && p->group()) {  // the slowest shard
+    double worst = -1.0;
+    for (const slsht_cuda_plan* q : p->parts) {
+      double ms = 0.0;
+      if (slsht_cuda_kernel_time(q, &ms) != SLSHT_OK) return SLSHT_ERR_VALIDATION;
+      worst = std::max(worst, ms);
+    }
+    *ms_out = worst;
+    return SLSHT_OK;
+  }
   if (!p || !ms_out || !p->lazy_valid) return SLSHT_ERR_VALIDATION;
   float ms = 0.f;
   if (cudaEventSynchronize(p->ev_lazy[1]) != cudaSuccess ||
@@ -1594,6 +1841,14 @@ int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int ba
     cleanup();
     g_create_error = st.msg;
     return st.code;
+  } catch (const CudaError& e) {  // CK / CKL: allocation or launch failure (memory ~ L^4)
+    cleanup();
+    g_create_error = e.msg;
+    return SLSHT_ERR_DEVICE;
+  } catch (const std::exception& e) {  // host vectors (mask samples, coefficients)
+    cleanup();
+    g_create_error = e.what();
+    return SLSHT_ERR_DEVICE;
   }
 }
 
@@ -1804,29 +2059,35 @@ int slsht_cuda_forward_direct(int device, int L_f, const double* f, int L_h, con
 }
 
 int slsht_cuda_delta_tables(int device, int L, double* out) {
-  slsht_cuda_plan* none = nullptr;
-  (void)none;
+  double* d = nullptr;
   try {
     if (L < 0) throw Status{SLSHT_ERR_VALIDATION, "band limit must be non-negative"};
+    if (!out) throw Status{SLSHT_ERR_VALIDATION, "null output"};
+    if (delta_smem(L) > 227 * 1024)  // checked before any allocation
+      throw Status{SLSHT_ERR_VALIDATION, "band limit too large for the on-chip Delta recursion"};
     int dev_count = 0;
     if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
       throw Status{SLSHT_ERR_DEVICE, "no CUDA device available (the engine has no CPU fallback)"};
     CK(cudaSetDevice(device));
     size_t dsz = 0;
     for (int pp = 0; pp <= L; ++pp) dsz += (size_t)(2 * pp + 1) * (2 * pp + 1);
-    double* d = dalloc<double>(dsz);
-    if ((size_t)(L + 1) * (L + 2) * 8 > 227 * 1024)
-      throw Status{SLSHT_ERR_VALIDATION, "band limit too large for the on-chip Delta recursion"};
+    d = dalloc<double>(dsz);
     CK(configure_delta(L));
     CK(launch_delta(L, d, 0));
     CK(cudaMemcpy(out, d, dsz * sizeof(double), cudaMemcpyDeviceToHost));
     CK(cudaFree(d));
     return SLSHT_OK;
   } catch (const Status& st) {
+    if (d) cudaFree(d);
     g_create_error = st.msg;
     return st.code;
   } catch (const CudaError& e) {
+    if (d) cudaFree(d);
     g_create_error = e.msg;
+    return SLSHT_ERR_DEVICE;
+  } catch (const std::exception& e) {
+    if (d) cudaFree(d);
+    g_create_error = e.what();
     return SLSHT_ERR_DEVICE;
   }
 }
@@ -1841,15 +2102,21 @@ int slsht_cuda_inverse(slsht_cuda_plan* p, const double* f, const double* h, dou
       throw Status{SLSHT_ERR_VALIDATION, "distribution lacks components up to L_f"};
     if (!f_rec) throw Status{SLSHT_ERR_VALIDATION, "null output"};
     const int rows = coeff_count(signal_band_limit);
+    // a multi-GPU plan gathers every shard's digest rows into its first shard's table (peer
+    // copies) and inverts there
+    slsht_cuda_plan* q = p->group() ? p->parts[0] : p;
+    CK(cudaSetDevice(q->desc.device));
     double* d_rec = dalloc<double>((size_t)2 * rows);
     try {
-      run_forward_device(p, f, h, 0, nullptr, 0, 0);
-      k_inverse<<<(rows + 127) / 128, 128, 0, p->stream>>>(
-          p->d_digest, signal_band_limit, p->real_mode && !p->emit_neg, h00_re, h00_im, d_rec);
+      if (p->group()) run_group_device(p, f, h, 0, q->d_digest, 1);
+      else run_forward_device(p, f, h, 0, nullptr, 0, 0);
+      CK(cudaSetDevice(q->desc.device));
+      k_inverse<<<(rows + 127) / 128, 128, 0, q->stream>>>(
+          q->d_digest, signal_band_limit, p->real_mode && !p->emit_neg, h00_re, h00_im, d_rec);
       CKL();
       CK(cudaMemcpyAsync(f_rec, d_rec, sizeof(double) * 2 * rows, cudaMemcpyDeviceToHost,
-                         p->stream));
-      check_numeric(p);
+                         q->stream));
+      check_numeric(q);
     } catch (...) {
       cudaFree(d_rec);
       throw;
@@ -1861,6 +2128,11 @@ int slsht_cuda_inverse(slsht_cuda_plan* p, const double* f, const double* h, dou
 int slsht_cuda_modulated(slsht_cuda_plan* p, const double* f, int count, const int* l,
                          const int* m, double* out) {
   if (!p) return SLSHT_ERR_VALIDATION;
+  if (p->group()) {  // every shard holds the whole modulated-SHT setup: the first one serves
+    const int rc = slsht_cuda_modulated(p->parts[0], f, count, l, m, out);
+    if (rc != SLSHT_OK) p->last_error = p->parts[0]->last_error;
+    return rc;
+  }
   return guarded(p, [&] {
     for (int i = 0; i < count; ++i)
       if (std::abs(m[i]) > l[i] || l[i] > p->L_g)
@@ -1872,28 +2144,37 @@ int slsht_cuda_modulated(slsht_cuda_plan* p, const double* f, int count, const i
       segs.push_back(Seg{m[i], l[i], l[i], i});
       tiles.push_back(MTile{m[i], i, 1});
     }
+    if (count <= 0) return;  // nothing requested: an empty result, no launch
     cudaStream_t s = p->stream;
+    struct Scratch {  // freed on every exit, errors included
+      Seg* ds = nullptr;
+      MTile* dt = nullptr;
+      double* A = nullptr;
+      double2* U = nullptr;
+      ~Scratch() {
+        cudaFree(ds);
+        cudaFree(dt);
+        cudaFree(A);
+        cudaFree(U);
+      }
+    } sc;
     CK(cudaMemcpyAsync(p->d_f, f, sizeof(double) * 2 * coeff_count(p->L_f), cudaMemcpyHostToDevice, s));
     run_setup(p);
-    Seg* ds = dupload(segs, s);
-    MTile* dt = dupload(tiles, s);
-    double* A = dalloc<double>((size_t)count * p->ldA);
-    double2* U = dalloc<double2>((size_t)count * p->NPQ);
+    sc.ds = dupload(segs, s);
+    sc.dt = dupload(tiles, s);
+    sc.A = dalloc<double>((size_t)count * p->ldA);
+    sc.U = dalloc<double2>((size_t)count * p->NPQ);
     k_agen<<<dim3(count, (p->ldA + 127) / 128), 128, 3 * (p->L_g + 1) * sizeof(double), s>>>(
-        ds, p->L_g, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_weights, A);
+        sc.ds, p->L_g, p->n_nodes, p->ldA, p->d_ncos, p->d_nsin, p->d_weights, sc.A);
     CKL();
     k_modgemm<<<dim3(count, (p->NPQ + MG_COLS - 1) / MG_COLS), 256, MG_SMEM, s>>>(
-        dt, p->n_nodes, p->ldA, p->L_f, p->NPQ, A, p->d_itab, p->d_lamh, p->d_pq, 0, 0, nullptr,
-        nullptr, U);
+        sc.dt, p->n_nodes, p->ldA, p->L_f, p->NPQ, sc.A, p->d_itab, p->d_lamh, p->d_pq, 0, 0, nullptr,
+        nullptr, sc.U);
     CKL();
     std::vector<double2> hU((size_t)count * p->NPQ);
-    CK(cudaMemcpyAsync(hU.data(), U, hU.size() * 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hU.data(), sc.U, hU.size() * 16, cudaMemcpyDeviceToHost, s));
     join_aux(p);
     CK(cudaStreamSynchronize(s));
-    cudaFree(ds);
-    cudaFree(dt);
-    cudaFree(A);
-    cudaFree(U);
     // back to the reference's triangular coeff_index(p, q) order, un-conjugated
     const int L = p->L_h;
     for (int i = 0; i < count; ++i) {

@@ -104,7 +104,9 @@ class Plan:
     def __init__(self, L_f: int, L_h: int, *, lmax: int = -1, real_mode: bool = False,
                  emit_negative_m: bool = True, device: int = 0, l_begin: int = 0,
                  l_end: int = -1, materialize: bool = False, ring_bytes: int = 0,
-                 stream: int | None = None):
+                 stream: int | None = None, devices: list[int] | None = None):
+        """devices: a multi-GPU plan, one balanced degree shard per entry (an ordinal may
+        repeat); the shards' digests are gathered into the caller's table."""
         self.lib = L.load()
         d = L.slsht_cuda_desc()
         d.L_f, d.L_h, d.lmax = L_f, L_h, lmax
@@ -112,6 +114,10 @@ class Plan:
         d.device, d.l_begin, d.l_end = device, l_begin, l_end
         d.materialize, d.ring_bytes = int(materialize), int(ring_bytes)
         d.stream = stream
+        if devices is not None and len(devices) > 1:
+            self._devices = (C.c_int * len(devices))(*devices)
+            d.n_devices = len(devices)
+            d.devices = self._devices
         handle = C.c_void_p()
         rc = self.lib.slsht_cuda_plan_create(C.byref(d), C.byref(handle))
         _raise(rc, None)
@@ -241,10 +247,27 @@ class Plan:
                 err.append(e)
 
         cfn = L.SINK(cb)
-        rc = self.lib.slsht_cuda_forward(self.handle, _dptr(f), _dptr(h), cfn, None)
+        rc = self.lib.slsht_cuda_forward(self.handle, _dptr(f), _dptr(h),
+                                         C.cast(cfn, C.c_void_p), None)
         if err:
             raise err[0]
         _raise(rc, self.handle)
+
+    def forward_copy(self, f: np.ndarray, h: np.ndarray, out: np.ndarray,
+                     first_index: int = 0) -> tuple[int, int]:
+        """Host-sink forward with the library's native copy sink (slsht_cuda_copy_sink): the
+        volume of (l, m) lands in out[coeff_index(l, m) - first_index] (out: [rows, n, L_h+1, n]
+        complex, C-contiguous). Returns (delivered, dropped)."""
+        f = np.ascontiguousarray(f, np.complex128)
+        h = np.ascontiguousarray(h, np.complex128)
+        if out.dtype != np.complex128 or not out.flags.c_contiguous:
+            raise ValidationError("out must be a C-contiguous complex128 array")
+        tgt = L.slsht_copy_target(out.ctypes.data, int(first_index), int(out.shape[0]),
+                                  int(self.volume_elems), 0, 0)
+        sink = C.cast(self.lib.slsht_cuda_copy_sink, C.c_void_p)
+        rc = self.lib.slsht_cuda_forward(self.handle, _dptr(f), _dptr(h), sink, C.byref(tgt))
+        _raise(rc, self.handle)
+        return int(tgt.delivered), int(tgt.dropped)
 
 
 def _real_mode(f: SphCoeffs, h: SphCoeffs, opts: ForwardOptions) -> bool:
@@ -279,6 +302,15 @@ def forward_fast(f: SphCoeffs, h: SphCoeffs, sink=None, opts: ForwardOptions | N
 
         plan.forward_sink(f.data, h.data, store)
         return SlshtDistribution(L_f, L_h, L_g, lmax, comps)
+
+
+def shard_bounds(l_begin: int, l_end: int, real_mode: bool, parts: int) -> list[int]:
+    """The degree shards of a multi-GPU plan (slsht_cuda_shard_bounds; host only)."""
+    lib = L.load()
+    out = (C.c_int * (parts + 1))()
+    rc = lib.slsht_cuda_shard_bounds(int(l_begin), int(l_end), int(real_mode), int(parts), out)
+    _raise(rc, None)
+    return list(out)
 
 
 def delta_tables(band_limit: int, device: int = 0) -> np.ndarray:

@@ -152,7 +152,7 @@ def make_roundtrip() -> None:
     # on R(pi/6, pi/6 + pi/240), random real f
     h, lam = R.eigenfunction_window(math.pi / 6.0, math.pi / 6.0 + math.pi / 240.0, 18, 4)
     arrays = {"h": h, "lambda": np.array(lam)}
-    for L_f in (18, 32):
+    for L_f in (18, 32, 48, 64):  # acceptance_main.cpp:87-107
         f = R.random_coeffs(L_f, 100 + L_f, True)
         arrays[f"f{L_f}"] = f
         arrays[f"frec{L_f}"] = R.roundtrip(f, L_f, True, h, 18, True)

@@ -1,6 +1,9 @@
-"""The multi-rank path on CPU (gloo, world size 2): degree shards computed independently and
-gathered to rank 0 with paper_1207_5558_b200.parallel.gather_digests must reproduce the
-one-rank result bit for bit (rows are copied, never reduced)."""
+"""The multi-rank path on CPU (gloo, world size 2): degree shards laid out by the engine's own
+shard rule (slsht_cuda_shard_bounds, the split of a multi-GPU plan) are computed independently
+(here by the CPU oracle: this container has no device; tests/test_gpu.py runs the same gather
+on engine-computed shards) and gathered to rank 0 with paper_1207_5558_b200.parallel.
+gather_digests; the result must reproduce the one-rank table bit for bit (rows are copied,
+never reduced)."""
 from __future__ import annotations
 
 import os
@@ -26,7 +29,7 @@ def _worker(rank, world, port, out_path):
     import torch.distributed as dist
 
     import oracle
-    from paper_1207_5558_b200 import configs as C
+    import paper_1207_5558_b200 as S
     from paper_1207_5558_b200.parallel import gather_digests
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -37,8 +40,8 @@ def _worker(rank, world, port, out_path):
     rng = np.random.default_rng(11)
     f = rng.standard_normal(49) + 1j * rng.standard_normal(49)
     h = rng.standard_normal(16) + 1j * rng.standard_normal(16)
-    cfg = C.Config(0, L_f, L_h, False, False, "test")
-    l0, l1 = C.shard_degrees(cfg, world, rank)
+    bounds = S.shard_bounds(0, L_f + L_h + 1, False, world)
+    l0, l1 = bounds[rank], bounds[rank + 1]
     local = torch.full(((L_f + L_h + 1) ** 2, 8), float("nan"), dtype=torch.float64)
     lm = [(l, m) for l in range(l0, l1) for m in range(-l, l + 1)]
     vols = O.components(f, L_f, h, L_h, lm)

@@ -32,6 +32,19 @@ def test_degree_shards_cover_and_balance(index, world):
     assert max(loads) - min(loads) <= 2 * w(cfg.L_g)
 
 
+@pytest.mark.parametrize("index", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_engine_shard_rule_equals_host_rule(index, world):
+    """slsht_cuda_shard_bounds (the multi-GPU plan's split, C ABI, host only) is the same rule as
+    configs.shard_degrees, which bench.py's ranks use."""
+    import paper_1207_5558_b200 as S
+
+    cfg = C.CONFIGS[index]
+    eng = S.shard_bounds(0, cfg.L_g + 1, cfg.real_mode, world)
+    host = [C.shard_degrees(cfg, world, r)[0] for r in range(world)] + [cfg.L_g + 1]
+    assert eng == host
+
+
 def test_config5_shards_match_survey_boundaries():
     cfg = C.CONFIGS[5]
     got = [C.shard_degrees(cfg, 8, r)[0] for r in range(8)] + [cfg.L_g + 1]
