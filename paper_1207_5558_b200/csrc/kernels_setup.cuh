@@ -314,14 +314,21 @@ __host__ __device__ __forceinline__ size_t wtile_index(int c, int col, int NPQ, 
 __global__ void k_wtab(int L, const double* __restrict__ h, const double* __restrict__ dtab,
                        const double2* __restrict__ rou, const int* __restrict__ pq_q,
                        int tile_nt, int ncol_pad, const int* __restrict__ wrow,
-                       double2* __restrict__ W) {
+                       double2* __restrict__ W, int fu_kp = 0) {
   const int n = 2 * L + 1, nb = L + 1, ncol = n * nb;
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   const int NPQ = (L + 1) * (L + 1);
   if (col >= ncol_pad) return;
+  // fu_kp > 0: the fused kernel's column-tile-major layout [col / 16][KR][16] with the K row
+  // wrow[c] of the interleaved row-group layout and XOR-swizzled columns (kernels_fused.cuh)
+  auto fused_index = [&](int cl) {
+    const int kr = wrow[c];
+    return ((size_t)(cl / 16) * fu_kp + kr) * 16 + ((cl & 8) | ((cl & 7) ^ ((2 * kr) & 7)));
+  };
   if (col >= ncol) {
-    W[wrow ? (size_t)wrow[c] * ncol_pad + col : wtile_index(c, col, NPQ, tile_nt)] =
+    W[fu_kp ? fused_index(col)
+            : wrow ? (size_t)wrow[c] * ncol_pad + col : wtile_index(c, col, NPQ, tile_nt)] =
         make_double2(0.0, 0.0);
     return;
   }
@@ -342,7 +349,8 @@ __global__ void k_wtab(int L, const double* __restrict__ h, const double* __rest
     ai += tr * z.y + ti * z.x;
   }
   // wrow: the two-pass GEMM's q-padded row layout with row stride ncol_pad
-  const size_t dst = wrow      ? (size_t)wrow[c] * ncol_pad + col
+  const size_t dst = fu_kp     ? fused_index(col)
+                     : wrow    ? (size_t)wrow[c] * ncol_pad + col
                      : tile_nt ? wtile_index(c, col, NPQ, tile_nt)
                                : (size_t)c * ncol + col;
   W[dst] = make_double2(ar, ai);

@@ -19,6 +19,7 @@
 #include "kernels_couple_ws.cuh"
 #include "kernels_couple_lines.cuh"
 #include "kernels_twopass.cuh"
+#include "kernels_fused.cuh"
 #include "direct.cuh"
 #include "window_solver.cuh"
 #include "kernels_setup.cuh"
@@ -126,6 +127,10 @@ struct slsht_cuda_plan {
   int tp_bn = 64;          //   k_tgemm column tile (32 in the overlapped schedule)
   int tp_gv = 3;           //   k_tgemm variant (tgemm_variant)
   bool tp_overlap = false; //   k_qfft + digest of chunk i on fft_stream under k_tgemm of i+1
+  bool use_fused = false;  // fused coupling (k_fused, n = 49): GEMM + FFT + epilogue in one
+  int fu_KP = 0, fu_upad = 0;
+  signed char* d_kend = nullptr;     // fused: [stage][row group] T row completed, or -1
+  unsigned char* d_kval = nullptr;   // fused: [stage][row group] k-step present
   bool tp_col_fast = false; //  k_tgemm raster: column tiles fastest (W L2-resident)
   bool tp_t_stream = false; //  k_tgemm: T stores with the evict-first hint
   size_t tp_t_elems = 0;   //   one T buffer (two in the overlapped schedule)
@@ -209,6 +214,8 @@ void free_plan(slsht_cuda_plan* p) {
   cudaFree(p->d_f);
   cudaFree(p->d_T);
   cudaFree(p->d_qend);
+  cudaFree(p->d_kend);
+  cudaFree(p->d_kval);
   cudaFree(p->d_wrow);
   cudaFree(p->d_r43);
   cudaFree(p->d_h);
@@ -407,6 +414,17 @@ void build_plan(slsht_cuda_plan* p) {
     if (p->tp_gv < 0 || p->tp_gv > 3) p->tp_gv = 3;
     p->tp_bn = tgemm_variant(p->tp_gv).bn;
   }
+  // fused coupling for n = 49 with SLSHT_CUDA_FUSED=1 (opt-in until it beats the two-pass
+  // path)
+  {
+    const char* e = std::getenv("SLSHT_CUDA_FUSED");
+    p->use_fused = p->n == 49 && e && e[0] == '1';
+    if (p->use_fused) {
+      p->use_tp = false;
+      p->fu_KP = FuCfg<49>::KR;
+      p->fu_upad = FuCfg<49>::UPAD;
+    }
+  }
   // ---- component list: orders m (all or m >= 0 in real mode), degrees in the shard
   for (int m = p->real_mode ? 0 : -p->lmax; m <= p->lmax; ++m) {
     const int lo = std::max(std::abs(m), p->l_begin), hi = std::min(p->lmax, p->l_end - 1);
@@ -452,6 +470,14 @@ void build_plan(slsht_cuda_plan* p) {
       }
       ch = best_b * TG_BM;
     }
+    if (p->use_fused && ch >= 8) {
+      // whole 8-component groups, a whole number of waves of the persistent CTAs when possible
+      int sms = 148;
+      if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device) != cudaSuccess)
+        sms = 148;
+      const long long groups = ch / 8;
+      ch = (groups >= sms ? groups / sms * sms : groups) * 8;
+    }
     p->max_chunk = (int)ch;
     p->n_slots = 2LL * per * ch;
   }
@@ -491,7 +517,9 @@ void build_plan(slsht_cuda_plan* p) {
     p->ws_stages.js[++cnt] = p->n;
     p->ws_stages.count = cnt;
   }
-  p->n_col_tiles = p->use_tp ? p->tp_ntiles : (p->ncol + 8 * p->NG - 1) / (8 * p->NG);
+  p->n_col_tiles = p->use_fused ? (p->ncol + FuCfg<49>::NT - 1) / FuCfg<49>::NT
+                   : p->use_tp  ? p->tp_ntiles
+                                : (p->ncol + 8 * p->NG - 1) / (8 * p->NG);
   const char* prof = std::getenv("SLSHT_CUDA_PROFILE");
   p->profile = prof && prof[0] == '1';
 
@@ -602,6 +630,38 @@ void build_plan(slsht_cuda_plan* p) {
     }
     p->ws_stages.group_elems = rows_pad;
   }
+  // ---- fused layout (k_fused, kernels_fused.cuh): T rows r = q mod n in G row groups
+  // (rows j + G k); each group's sequence of k-steps (its rows in order, every row padded to
+  // whole k-steps) is interleaved across the groups: K row ((s G + j) 4 + kl) holds position
+  // 4 s + kl of group j's sequence. U (8-component groups, row stride UPAD) and W use it.
+  std::vector<signed char> kend;
+  std::vector<unsigned char> kval;
+  if (p->use_fused) {
+    using FC = FuCfg<49>;
+    wrow.assign(p->NPQ, 0);
+    kend.assign((size_t)FC::NST * FC::G, (signed char)-1);
+    kval.assign((size_t)FC::NST * FC::G, 0);
+    for (int j = 0; j < FC::G; ++j) {
+      int pos = 0;
+      for (int k = 0; k < FC::R1; ++k) {
+        const int r = j + FC::G * k;              // T row = q mod n
+        const int q = r <= L ? r : r - p->n;
+        const int jq = q + L;
+        for (int c = qoff[jq]; c < qoff[jq + 1]; ++c, ++pos) {
+          const int s0 = pos / 4, kl = pos % 4;
+          wrow[c] = (s0 * FC::G + j) * 4 + kl;
+          ubase[c] = wrow[c];
+          ustr[c] = p->fu_upad;
+        }
+        pos = (pos + 3) / 4 * 4;
+        kend[(size_t)(pos / 4 - 1) * FC::G + j] = (signed char)r;
+      }
+      for (int s0 = 0; s0 < pos / 4; ++s0) kval[(size_t)s0 * FC::G + j] = 1;
+      if (pos / 4 > FC::NST)
+        throw Status{SLSHT_ERR_VALIDATION, "internal: fused K layout mismatch"};
+    }
+    p->ws_stages.group_elems = 8LL * p->fu_upad;
+  }
   // ---- alpha-axis FFT plan: roots of unity, DIF stages, output permutation, phase shift
   const int n = p->n;
   std::vector<double2> rou(n), phase(n);
@@ -698,7 +758,14 @@ void build_plan(slsht_cuda_plan* p) {
   p->d_dtab = dalloc<double>(dsz * p->nb);
   const int tile_nt_alloc = p->use_lines ? 8 : (p->use_ws ? p->ws.NT : 0);
   const size_t ncol_pad = tile_nt_alloc ? (size_t)p->n_col_tiles * tile_nt_alloc : (size_t)p->ncol;
-  if (p->use_tp) {
+  if (p->use_fused) {
+    const size_t welems = (size_t)p->n_col_tiles * p->fu_KP * FuCfg<49>::NT;
+    p->d_W = dalloc<double2>(welems);
+    CK(cudaMemsetAsync(p->d_W, 0, welems * 16, s));  // padding rows
+    p->d_wrow = dupload(wrow, s);
+    p->d_kend = dupload(kend, s);
+    p->d_kval = dupload(kval, s);
+  } else if (p->use_tp) {
     p->d_W = dalloc<double2>((size_t)p->tp_KP * p->tp_ncolp);
     CK(cudaMemsetAsync(p->d_W, 0, (size_t)p->tp_KP * p->tp_ncolp * 16, s));  // padding rows
     p->d_wrow = dupload(wrow, s);
@@ -725,7 +792,11 @@ void build_plan(slsht_cuda_plan* p) {
   p->d_segs = dupload(p->segs, s);
   p->d_tiles = dupload(p->tiles, s);
   p->d_A = dalloc<double>((size_t)p->max_chunk * p->ldA);
-  if (p->use_tp) {
+  if (p->use_fused) {
+    const size_t uelems = (size_t)(p->max_chunk + 7) / 8 * 8 * p->fu_upad;
+    p->d_U = dalloc<double2>(uelems);
+    CK(cudaMemsetAsync(p->d_U, 0, uelems * 16, s));  // padding rows stay zero
+  } else if (p->use_tp) {
     p->d_U = dalloc<double2>((size_t)p->max_chunk * p->tp_KP);
     CK(cudaMemsetAsync(p->d_U, 0, (size_t)p->max_chunk * p->tp_KP * 16, s));  // padding rows
   } else if (p->use_ws || p->use_lines) {
@@ -755,7 +826,8 @@ void build_plan(slsht_cuda_plan* p) {
                  "device output buffer does not fit in HBM (use the streaming ring mode)"};
   p->d_out = dalloc<double2>((size_t)p->n_slots * p->vol);
   if (p->use_tp) p->d_T = dalloc<double2>(t_bytes / 16);
-  p->d_partials = dalloc<double>((size_t)p->max_chunk * p->n_col_tiles * 8);
+  const int parts_per_tile = p->use_fused ? FuCfg<49>::EPW : 1;
+  p->d_partials = dalloc<double>((size_t)p->max_chunk * p->n_col_tiles * parts_per_tile * 8);
   p->digest_rows = coeff_count(p->lmax);
   p->d_digest = dalloc<double>((size_t)p->digest_rows * 8);
   for (int i = 0; i < 2; ++i) {
@@ -774,7 +846,11 @@ void build_plan(slsht_cuda_plan* p) {
     if (pq[2 * c1] - pq[2 * c0] + 1 > MG_NQ)
       throw Status{SLSHT_ERR_VALIDATION, "internal: column tile spans too many orders q"};
   }
-  if (p->use_lines) {
+  if (p->use_fused) {
+    p->couple_smem = FuCfg<49>::SMEM;
+    CK(cudaFuncSetAttribute(k_fused<49>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)p->couple_smem));
+  } else if (p->use_lines) {
     CK(cudaFuncSetAttribute(p->lines_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)p->couple_smem));
   } else if (p->use_tp) {
@@ -906,10 +982,12 @@ void run_setup(slsht_cuda_plan* p) {
   k_dtab<<<dim3((wmax + 255) / 256, L + 1), 256, 0, a>>>(L, p->d_delta, p->d_rou, p->d_dtab);
   CKL();
   const int tile_nt = p->use_lines ? 8 : (p->use_ws ? p->ws.NT : 0);
-  const int ncol_pad = p->use_tp ? p->tp_ncolp : (tile_nt ? p->n_col_tiles * tile_nt : p->ncol);
+  const int ncol_pad = p->use_fused ? p->n_col_tiles * FuCfg<49>::NT
+                       : p->use_tp  ? p->tp_ncolp
+                                    : (tile_nt ? p->n_col_tiles * tile_nt : p->ncol);
   k_wtab<<<dim3((ncol_pad + 127) / 128, p->NPQ), 128, 0, a>>>(
-      L, p->d_h, p->d_dtab, p->d_rou, p->d_pq, tile_nt, ncol_pad, p->use_tp ? p->d_wrow : nullptr,
-      p->d_W);
+      L, p->d_h, p->d_dtab, p->d_rou, p->d_pq, tile_nt, ncol_pad,
+      (p->use_tp || p->use_fused) ? p->d_wrow : nullptr, p->d_W, p->use_fused ? p->fu_KP : 0);
   CKL();
   CK(cudaEventRecord(p->ev_wtab, a));
   p->wtab_pending = true;
@@ -929,7 +1007,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   record(p, 1);
   k_modgemm<<<dim3(ch.ntile, (p->NPQ + MG_COLS - 1) / MG_COLS), 256, MG_SMEM, s>>>(
       p->d_tiles + ch.tile0, p->n_nodes, p->ldA, p->L_f, p->NPQ, p->d_A, p->d_itab, p->d_lamh,
-      p->d_pq, p->use_lines ? 8 : (p->use_ws ? p->ws.MT : (p->use_tp ? 1 : 0)),
+      p->d_pq, (p->use_lines || p->use_fused) ? 8 : (p->use_ws ? p->ws.MT : (p->use_tp ? 1 : 0)),
       p->ws_stages.group_elems,
       p->d_ubase, p->d_ustr, p->d_U);
   CKL();
@@ -959,7 +1037,26 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   prm.fft = p->fft;
   prm.generic_dft = p->generic_dft;
   const int MT = 8 * p->MG;
-  if (p->use_lines) {
+  if (p->use_fused) {
+    FuParams fp{};
+    fp.U = p->d_U;
+    fp.W = p->d_W;
+    fp.out = p->d_out;
+    fp.partials = p->d_partials;
+    fp.comps = comps;
+    fp.count = ch.count;
+    fp.n_groups = (ch.count + 7) / 8;
+    fp.n_col_tiles = p->n_col_tiles;
+    fp.ncol = p->ncol;
+    fp.vol = p->vol;
+    fp.mirror = p->mirror;
+    fp.rou = p->d_rou;
+    fp.betaw = p->d_betaw;
+    fp.kend = p->d_kend;
+    fp.kval = p->d_kval;
+    const int grid = std::min(fp.n_groups, p->num_sms);
+    k_fused<49><<<grid, FuCfg<49>::NTHREADS, p->couple_smem, s>>>(fp);
+  } else if (p->use_lines) {
     LnParams lp{};
     lp.c = prm;
     lp.group_elems = p->ws_stages.group_elems;
@@ -1110,7 +1207,9 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   record(p, 3);
   record_lazy(p, 1);
   k_digest<<<(ch.count + 3) / 4, 128, 0, s>>>(comps, ch.count,
-                                                  p->use_lines ? p->lines_nseg_dig : p->n_col_tiles,
+                                                  p->use_lines   ? p->lines_nseg_dig
+                                                  : p->use_fused ? p->n_col_tiles * FuCfg<49>::EPW
+                                                                 : p->n_col_tiles,
                                                   p->n, p->d_partials, p->mirror, p->d_digest);
   CKL();
   record(p, 4);
@@ -1263,7 +1362,8 @@ void run_group_device(slsht_cuda_plan* p, const double* f, const double* h, int 
   p->launches = 0;
   for (slsht_cuda_plan* q : p->parts) {
     CK(cudaSetDevice(q->desc.device));
-    run_forward_device(q, f, h, inputs_on_device, digests, digests_on_device, 0);
+    run_forward_device(q, f, h, inputs_on_device, nullptr, 0, 0);
+    if (digests) copy_digests(q, digests, digests_on_device != 0);
   }
   for (slsht_cuda_plan* q : p->parts) {
     CK(cudaSetDevice(q->desc.device));
