@@ -7,11 +7,24 @@
 namespace slsht_cuda {
 
 // ---------------------------------------------------------------------------------------------
-// A[row][j] = w_j lambda_l^m(theta_j) for the rows l0..l1 of one order-m segment.
+// A[row][j] = w_j lambda_l^m(x_j) for the rows l0..l1 of one order-m segment, on the x >= 0
+// Gauss-Legendre nodes (kernels_setup.cuh). The segment's rows are stored parity-sorted: first
+// the degrees with l + m even, then the odd ones (each in increasing l), so every GEMM tile has
+// one parity class and selects I_0 or I_1 per column (k_modgemm).
 // grid (segments, node blocks of 128); dynamic smem 3 (L_g+1) doubles of recursion coefficients.
 struct Seg {
   int m, l0, l1, row0;
 };
+
+__host__ __device__ __forceinline__ int seg_even_first(int m, int l0) {
+  return ((l0 + m) & 1) ? l0 + 1 : l0;
+}
+// A row (within the segment) of degree l
+__host__ __device__ __forceinline__ int seg_arow(int m, int l0, int l1, int l) {
+  const int e0 = seg_even_first(m, l0);
+  const int ne = e0 <= l1 ? (l1 - e0) / 2 + 1 : 0;
+  return ((l + m) & 1) ? ne + (l - (e0 == l0 ? l0 + 1 : l0)) / 2 : (l - e0) / 2;
+}
 
 __global__ void __launch_bounds__(128) k_agen(const Seg* __restrict__ segs, int L_g, int n_nodes,
                                               int ldA, const double* __restrict__ ncos,
@@ -36,15 +49,17 @@ __global__ void __launch_bounds__(128) k_agen(const Seg* __restrict__ segs, int 
   while (r.l < s.l0) r.next(ca, cb);
   for (int l = s.l0; l <= s.l1; ++l) {
     if (l > s.l0) r.next(ca, cb);
-    A[(size_t)(s.row0 + l - s.l0) * ldA + j] = wj * r.cur;
+    A[(size_t)(s.row0 + seg_arow(s.m, s.l0, s.l1, l)) * ldA + j] = wj * r.cur;
   }
 }
 
 // ---------------------------------------------------------------------------------------------
 // The modulated SHT (transform.cpp:189-220) of every row of one order m as a GEMM on the FP64
-// tensor cores:
-//   mod[row][c] = sum_j A[row][j] * B_m[j][c],  B_m[j][c] = I(theta_j, m - q_c) lambda_c(theta_j)
-// (zero where |m - q_c| > L_f), c in q-major (p, q) order. U = conj(mod) is stored.
+// tensor cores, over the x >= 0 Gauss-Legendre nodes (kernels_setup.cuh):
+//   mod[row][c] = sum_j A[row][j] * B_m[j][c],  B_m[j][c] = I_s(x_j, m - q_c) lambda_c(x_j),
+//   s = parity of the tile's rows (l + m) xor parity of p_c + q_c
+// (zero where |m - q_c| > L_f), c in q-major (p, q) order. U = conj(mod) is stored at the
+// tile's natural rows nat0 + 2 r (the A rows are parity-sorted, k_agen).
 // CTA tile 32 rows x 64 complex columns, K chunks of 32 nodes, 8 warps = 2 row groups x 4
 // column groups, each warp 16 rows x 16 complex columns = 8 DMMA per k-step of 4.
 // Operands stream through a two-stage cp.async pipeline: the A rows, the raw lambda_c rows
@@ -52,7 +67,8 @@ __global__ void __launch_bounds__(128) k_agen(const Seg* __restrict__ segs, int 
 // MMA, two multiplies per fragment). A, lambda and I rows have the padded node stride ldA
 // (zeros past n_nodes), so every copy is a whole 16-B chunk.
 struct MTile {
-  int m, row0, rows;
+  int m, row0, rows;  // order, first A row, rows (one parity class)
+  int nat0, par;      // natural (chunk) row of tile row 0 (stride 2), parity of l + m
 };
 
 constexpr int MG_ROWS = 32;  // rows per CTA tile
@@ -61,7 +77,7 @@ constexpr int MG_K = 32;     // nodes per K chunk
 constexpr int MG_NQ = 16;    // distinct q per column tile (host-checked)
 constexpr int MG_KS = MG_K + 4;  // padded row stride of the A and lambda stages (doubles)
 constexpr size_t MG_STAGE = (size_t)MG_ROWS * MG_KS * 8 + (size_t)MG_COLS * MG_KS * 8 +
-                            (size_t)MG_K * MG_NQ * 16;
+                            (size_t)MG_K * MG_NQ * 2 * 16;
 constexpr size_t MG_SMEM = 2 * MG_STAGE;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
@@ -80,7 +96,7 @@ __device__ __forceinline__ void cp_async_wait() {
 
 template <int RG>
 __device__ __forceinline__ void modgemm_tile(const MTile t, int n_nodes, int ldA, int L_f,
-                                             int NPQ, const int* colq,
+                                             int NPQ, const int* colq, const int* colpar,
                                              const double* __restrict__ A,
                                              const double2* __restrict__ itab,
                                              const double* __restrict__ lamh, int u_group,
@@ -120,11 +136,12 @@ __device__ __forceinline__ void modgemm_tile(const MTile t, int n_nodes, int ldA
       cp_async16(Ls + cc * MG_KS + 2 * u, lamh + (size_t)(ok ? cbase + cc : 0) * ldA + k0 + 2 * u, ok);
     }
 #pragma unroll
-    for (int i = 0; i < MG_K * MG_NQ / 256; ++i) {
-      const int e = tid + 256 * i, k = e % MG_K, sq = e / MG_K;
+    for (int i = 0; i < MG_K * MG_NQ * 2 / 256; ++i) {  // Is[k][sq][s] = I_s(x_k, m - q)
+      const int e = tid + 256 * i, k = e % MG_K, sqs = e / MG_K, sq = sqs >> 1;
       const int mu = t.m - (q_lo + sq);
       const bool ok = sq < nq && mu >= -L_f && mu <= L_f;
-      cp_async16(Is + k * MG_NQ + sq, itab + (size_t)(ok ? mu + L_f : 0) * ldA + k0 + k, ok);
+      cp_async16(Is + k * MG_NQ * 2 + sqs,
+                 itab + (size_t)(ok ? 2 * (mu + L_f) + (sqs & 1) : 0) * ldA + k0 + k, ok);
     }
     cp_async_commit();
   };
@@ -135,9 +152,12 @@ __device__ __forceinline__ void modgemm_tile(const MTile t, int n_nodes, int ldA
     for (int b = 0; b < CF; ++b)
 #pragma unroll
       for (int c = 0; c < 2; ++c) acc[a][b][c][0] = acc[a][b][c][1] = 0.0;
-  int qi[CF];
+  int qi[CF];  // the column's I entry in a stage: 2 (q - q_lo) + s
 #pragma unroll
-  for (int cf = 0; cf < CF; ++cf) qi[cf] = colq[cgp * 8 * CF + cf * 8 + (lane >> 2)] - q_lo;
+  for (int cf = 0; cf < CF; ++cf) {
+    const int col = cgp * 8 * CF + cf * 8 + (lane >> 2);
+    qi[cf] = 2 * (colq[col] - q_lo) + (colpar[col] ^ t.par);
+  }
   const int nchunks = ldA / MG_K;
   issue(0, 0);
   for (int ch = 0; ch < nchunks; ++ch) {
@@ -165,7 +185,7 @@ __device__ __forceinline__ void modgemm_tile(const MTile t, int n_nodes, int ldA
           for (int cf = 0; cf < CF; ++cf) {
             const int col = cgp * 8 * CF + cf * 8 + (lane >> 2);
             const double lv = Ls[col * MG_KS + k];
-            const double2 iv = Is[k * MG_NQ + qi[cf]];
+            const double2 iv = Is[k * MG_NQ * 2 + qi[cf]];
             const double br = iv.x * lv, bi = iv.y * lv;
             dmma(acc[0][cf][0][0], acc[0][cf][0][1], a0, br);
             dmma(acc[0][cf][1][0], acc[0][cf][1][1], a0, bi);
@@ -187,7 +207,7 @@ __device__ __forceinline__ void modgemm_tile(const MTile t, int n_nodes, int ldA
       for (int e = 0; e < 2; ++e) {
         const int c = cbase + cgp * 8 * CF + cf * 8 + 2 * (lane & 3) + e;
         if (c < NPQ) {
-          const int row = t.row0 + r;
+          const int row = t.nat0 + 2 * r;
           // u_group == 0: U[row][c]; else the stage-tiled layout of the warp-specialized
           // coupling kernel: group row / MT, stage block u_base[c], row stride u_str[c]
           const size_t dst = u_group ? (size_t)(row / u_group) * u_gs + u_base[c] +
@@ -211,16 +231,22 @@ __global__ void __launch_bounds__(256) k_modgemm(const MTile* __restrict__ tiles
                                                  const int* __restrict__ u_base,
                                                  const int* __restrict__ u_str,
                                                  double2* __restrict__ U) {
-  __shared__ int colq[MG_COLS];
+  __shared__ int colq[MG_COLS], colpar[MG_COLS];  // q and the parity of p + q per column
   const int cbase = blockIdx.y * MG_COLS;
-  if (threadIdx.x < MG_COLS)
-    colq[threadIdx.x] = (cbase + (int)threadIdx.x < NPQ) ? pq_q[2 * (cbase + threadIdx.x)] : 0;
+  if (threadIdx.x < MG_COLS) {
+    const bool in = cbase + (int)threadIdx.x < NPQ;
+    const int c = in ? cbase + threadIdx.x : 0;
+    colq[threadIdx.x] = in ? pq_q[2 * c] : 0;
+    colpar[threadIdx.x] = in ? ((pq_q[2 * c] + pq_q[2 * c + 1]) & 1) : 0;
+  }
   __syncthreads();
   const MTile t = tiles[blockIdx.x];
   if (t.rows <= 16)
-    modgemm_tile<1>(t, n_nodes, ldA, L_f, NPQ, colq, A, itab, lamh, u_group, u_gs, u_base, u_str, U);
+    modgemm_tile<1>(t, n_nodes, ldA, L_f, NPQ, colq, colpar, A, itab, lamh, u_group, u_gs, u_base,
+                    u_str, U);
   else
-    modgemm_tile<2>(t, n_nodes, ldA, L_f, NPQ, colq, A, itab, lamh, u_group, u_gs, u_base, u_str, U);
+    modgemm_tile<2>(t, n_nodes, ldA, L_f, NPQ, colq, colpar, A, itab, lamh, u_group, u_gs, u_base,
+                    u_str, U);
 }
 
 // ---------------------------------------------------------------------------------------------

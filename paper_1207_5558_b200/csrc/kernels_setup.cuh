@@ -34,27 +34,154 @@ __device__ __forceinline__ void quad_weight_sum(int K, double angle, int lane, d
   }
 }
 
-// The main-stream setup in one launch. Three independent parts, each computing the node
-// angles it needs with the same expression (so the values are identical), run side by side:
-//   blocks [0, ni): the I-table I(theta_j, mu) = 2 pi conj(sum_l f_l^mu lambda_l^mu(theta_j))
-//     (transform.cpp:158-173), per (node block, order mu), recursion coefficients and f_l^mu
-//     staged in shared memory;
+// ---------------------------------------------------------------------------------------------
+// The theta quadrature of the modulated SHT. The reference integrates over theta with the
+// exact rule of S_{2L_g} (theta_weights(2L_g) on N_theta = 2L_g + 1 nodes, transform.cpp:
+// 151-156, 206-219). The integrand lambda_{l'}^{m-q} lambda_l^m lambda_p^q (l' <= L_f, l <= L_g,
+// p <= L_h) is sin(theta) times a polynomial in x = cos(theta) of degree <= l' + l + p <=
+// 2 L_g (the three orders sum to zero, so the sin powers pair up), so the (L_g + 1)-point
+// Gauss-Legendre rule in x is exact for it too: the same integral, on fewer nodes, equal to
+// the reference's up to roundoff (~1e-13 relative; tests/test_gpu.py). The GL nodes are
+// symmetric, x <-> -x, and lambda_l^m(-x) = (-1)^(l+m) lambda_l^m(x), so the engine keeps only
+// the nodes with x >= 0 and folds the mirrored node into the I-table:
+//   mod_p^q(l, m) = sum_{x_j >= 0} w_j lambda_l^m lambda_p^q I_s(x_j, m - q),
+//   s = (l + m + p + q) mod 2, I_0 = I(x) + I(-x), I_1 = I(x) - I(-x)
+// (the x = 0 node of an odd rule enters with half its weight; there I_1 = 0 and I_0 = 2 I).
+// Half the nodes again, so the modulated-SHT GEMM does a quarter of the reference rule's work.
+//
+// k_glnodes: node j < K (the j-th root of P_NG from theta = 0) by Newton's method in theta,
+// from Tricomi's asymptotic guess x = (1 - 1/(8 NG^2) + 1/(8 NG^3)) cos(pi (j + 3/4) /
+// (NG + 1/2)) (error O(NG^-4): one or two steps reach full precision). Near the pole x = cos
+// theta carries theta only to eps / sin(theta), so P_NG is evaluated through y = 1 - x =
+// 2 sin^2(theta / 2), exact to an ulp at every theta, with the recursion on the differences
+//   D_k = P_k - P_{k-1} = b_k D_{k-1} - a_k y P_{k-1},   a_k = (2k - 1)/k, b_k = (k - 1)/k
+// (shared tables, no division in the dependent chain). A node from x-space Newton steps is off
+// by up to ~1e-14 rad near the pole, which at l = L_g costs ~1e-13 relative in the modulated
+// SHT (measured in long double at config 5, (l, m) = (1088, 0)). dP_NG/dtheta = NG (D_NG -
+// y P_NG) / sin(theta). The weight w = 2 sin^2(theta) / (NG (D_NG - y P_NG))^2 needs the
+// recursion to full precision (double loses ~NG ulps: 6e-13 rms at NG = 1089): for large NG
+// the last evaluation runs in double-double arithmetic (a_k, b_k as double-double pairs). One thread
+// per node; dynamic smem 4 (NG + 1) doubles.
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD dd_fast2sum(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  return DD{s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  const double s = __dadd_rn(a.hi, b.hi), v = __dsub_rn(s, a.hi);
+  double e = __dadd_rn(__dsub_rn(a.hi, __dsub_rn(s, v)), __dsub_rn(b.hi, v));
+  e = __dadd_rn(e, __dadd_rn(a.lo, b.lo));
+  return dd_fast2sum(s, e);
+}
+__device__ __forceinline__ DD dd_mul(DD a, DD b) {
+  const double p = __dmul_rn(a.hi, b.hi);
+  double e = fma(a.hi, b.hi, -p);
+  e = fma(a.hi, b.lo, e);
+  e = fma(a.lo, b.hi, e);
+  return dd_fast2sum(p, e);
+}
+__device__ __forceinline__ DD dd_mul_d(DD a, double b) {
+  const double p = __dmul_rn(a.hi, b);
+  double e = fma(a.hi, b, -p);
+  e = fma(a.lo, b, e);
+  return dd_fast2sum(p, e);
+}
+
+__global__ void k_glnodes(int NG, int K, double* __restrict__ ncos, double* __restrict__ nsin,
+                          double* __restrict__ weights) {
+  extern __shared__ double tb[];  // [k][4]: a_k, its residual, b_k, its residual
+  for (int k = 2 + threadIdx.x; k <= NG; k += blockDim.x) {
+    const double a = (double)(2 * k - 1) / k, b = (double)(k - 1) / k;
+    tb[4 * k] = a;
+    tb[4 * k + 1] = fma(-a, (double)k, (double)(2 * k - 1)) / k;
+    tb[4 * k + 2] = b;
+    tb[4 * k + 3] = fma(-b, (double)k, (double)(k - 1)) / k;
+  }
+  __syncthreads();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= K) return;
+  // P_NG and D_NG at y (double)
+  auto eval = [&](double y, double& pn, double& dn) {
+    double p = 1.0 - y, d = -y;  // P_1, D_1
+    for (int k = 2; k <= NG; ++k) {
+      d = fma(tb[4 * k + 2], d, -(tb[4 * k] * y) * p);
+      p += d;
+    }
+    pn = p;
+    dn = d;
+  };
+  const double g = (double)NG;
+  const bool mid = 2 * j + 1 == NG;  // the middle node of an odd rule: x = 0 exactly
+  double th = 0.5 * kPi;
+  if (!mid) {
+    th = acos((1.0 - 1.0 / (8.0 * g * g) + 1.0 / (8.0 * g * g * g)) *
+              cos(kPi * (j + 0.75) / (g + 0.5)));
+    for (int it = 0; it < 10; ++it) {
+      const double sh = sin(0.5 * th), y = 2.0 * sh * sh;
+      double pn, dn;
+      eval(y, pn, dn);
+      const double d = pn * sin(th) / (g * (dn - y * pn));  // P_NG / (dP_NG / dtheta)
+      th -= d;
+      if (fabs(d) < 1e-14) break;
+    }
+  }
+  double c, s;
+  sincos(th, &s, &c);
+  double y;
+  if (mid) {
+    c = 0.0;
+    s = 1.0;
+    y = 1.0;
+  } else {
+    const double sh = sin(0.5 * th);
+    y = 2.0 * sh * sh;
+  }
+  // the weight's P_NG, D_NG: in double-double above NG = 256 (below, the double recursion's
+  // ~NG ulps stay under the other roundoff of the modulated SHT: 1.5e-14 rms at NG = 145)
+  double dv;
+  if (NG > 256) {
+    DD p{1.0, 0.0}, d{-y, 0.0};
+    p = dd_add(p, d);
+    for (int k = 2; k <= NG; ++k) {
+      const DD ay = dd_mul_d(DD{tb[4 * k], tb[4 * k + 1]}, y);
+      const DD t = dd_mul(ay, p);
+      d = dd_add(dd_mul(DD{tb[4 * k + 2], tb[4 * k + 3]}, d), DD{-t.hi, -t.lo});
+      p = dd_add(p, d);
+    }
+    const DD yp = dd_mul_d(p, y);
+    const DD den = dd_add(d, DD{-yp.hi, -yp.lo});  // D_NG - y P_NG = x P_NG - P_{NG-1}
+    dv = g * (den.hi + den.lo);
+  } else {
+    double pn, dn;
+    eval(y, pn, dn);
+    dv = g * (dn - y * pn);
+  }
+  double w = 2.0 * s * s / (dv * dv);
+  if (mid) w *= 0.5;
+  ncos[j] = c;
+  nsin[j] = s;
+  weights[j] = w;
+}
+
+// The main-stream setup in one launch. Three independent parts run side by side:
+//   blocks [0, ni): the I-table per (node block, order mu), recursion coefficients and f_l^mu
+//     staged in shared memory: I_0 and I_1 (above) of I(theta_j, mu) = 2 pi conj(sum_l f_l^mu
+//     lambda_l^mu(theta_j)) (transform.cpp:158-173), rows 2 (mu + L_f) + s;
 //   blocks [ni, ni + nw): the window rows lambda_p^q(theta_j), q-major (p, q) rows
 //     c = qoff[q+L] + p-|q| (transform.cpp:175-186), per (node block, order q);
-//   the rest: theta nodes and weights, beta weights (4 warps = 4 weights per block).
-// Row strides are ld (>= n_nodes, the padding stays zero).
+//   the rest: theta_weights(2 L_g) of the reference rule, for its imaginary-residue check
+//     (grids.cpp:86-89: NumericError), and beta weights (4 warps = 4 weights per block).
+// The GL nodes come from k_glnodes. Row strides are ld (>= n_nodes, the padding stays zero).
 struct SetupMainParams {
   int N, L_h, L_f, n_nodes, ld, nbx, ni, nw;
   const double* f;
   const int* qoff;
-  double *ncos, *nsin, *weights, *betaw, *lamh, *itab;
+  const double *ncos, *nsin;
+  double *betaw, *lamh, *itab;
   int* err;
 };
-
-__device__ __forceinline__ void node_angle(int N, int j, double& c, double& s) {
-  const double theta = kPi * (2 * j + 1) / (2 * N + 1);
-  sincos(theta, &s, &c);
-}
 
 __global__ void __launch_bounds__(128) k_setup_main(const SetupMainParams P) {
   extern __shared__ double coef[];
@@ -71,21 +198,22 @@ __global__ void __launch_bounds__(128) k_setup_main(const SetupMainParams P) {
     __syncthreads();
     const int j = (b % P.nbx) * blockDim.x + threadIdx.x;
     if (j >= P.n_nodes) return;
-    double c, s;
-    node_angle(P.N, j, c, s);
     LegendreIt r;
-    r.seed(mu, c, s, sf);
-    double ar = 0.0, ai = 0.0;
+    r.seed(mu, P.ncos[j], P.nsin[j], sf);
+    // [parity of l + mu][re, im]: the even terms make I_0 / 2, the odd ones I_1 / 2
+    double a[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     for (int l = amu; l <= L_f; ++l) {
       if (l > amu) r.next(ca, cb);
       const double2 fv = fs[l];
-      ar += fv.x * r.cur;
-      ai += fv.y * r.cur;
+      const int s = (l + amu) & 1;
+      a[s][0] += fv.x * r.cur;
+      a[s][1] += fv.y * r.cur;
     }
-    double2 o;
-    o.x = 2.0 * kPi * ar;
-    o.y = -(2.0 * kPi * ai);
-    reinterpret_cast<double2*>(P.itab)[(size_t)(mu + L_f) * P.ld + j] = o;
+    double2* it = reinterpret_cast<double2*>(P.itab);
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+      it[(size_t)(2 * (mu + L_f) + s) * P.ld + j] =
+          make_double2(4.0 * kPi * a[s][0], -(4.0 * kPi * a[s][1]));
     return;
   }
   b -= P.ni;
@@ -98,10 +226,8 @@ __global__ void __launch_bounds__(128) k_setup_main(const SetupMainParams P) {
     __syncthreads();
     const int j = (b % P.nbx) * blockDim.x + threadIdx.x;
     if (j >= P.n_nodes) return;
-    double c, s;
-    node_angle(P.N, j, c, s);
     LegendreIt r;
-    r.seed(q, c, s, sf);
+    r.seed(q, P.ncos[j], P.nsin[j], sf);
     const int base = P.qoff[q + L_h];
     for (int p = aq; p <= L_h; ++p) {
       if (p > aq) r.next(ca, cb);
@@ -110,22 +236,15 @@ __global__ void __launch_bounds__(128) k_setup_main(const SetupMainParams P) {
     return;
   }
   b -= P.nw;
-  // ---- quadrature weights and node angles: one warp per weight (as k_nodes)
+  // ---- the reference rule's theta weights (only their residue check is used) and the beta
+  // weights: one warp per weight
   const int N = P.N, L_h = P.L_h;
   const int w = (b * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w <= N) {
-    const int t = w;
-    const double theta = kPi * (2 * t + 1) / (2 * N + 1);
+    const double theta = kPi * (2 * w + 1) / (2 * N + 1);
     double sr, si;
     quad_weight_sum(N, theta, lane, sr, si);
-    if (lane == 0) {
-      double s, c;
-      sincos(theta, &s, &c);
-      P.ncos[t] = c;
-      P.nsin[t] = s;
-      if (fabs(si) >= 1e-12) atomicExch(P.err, 1);
-      P.weights[t] = (t < N) ? 2.0 * sr / (2 * N + 1) : sr / (2 * N + 1);
-    }
+    if (lane == 0 && fabs(si) >= 1e-12) atomicExch(P.err, 1);
   } else if (w - (N + 1) <= L_h) {
     const int t = w - (N + 1);
     const int L = L_h, n = 2 * L + 1;

@@ -396,8 +396,8 @@ void build_plan(slsht_cuda_plan* p) {
   p->nb = L + 1;
   p->ncol = p->n * p->nb;
   p->NPQ = (L + 1) * (L + 1);
-  p->N = 2 * p->L_g;
-  p->n_nodes = p->N + 1;
+  p->N = 2 * p->L_g;                // the reference rule S_{2L_g} (its residue check only)
+  p->n_nodes = (p->L_g + 2) / 2;    // x >= 0 half of the (L_g + 1)-point Gauss-Legendre rule
   p->ldA = (p->n_nodes + MG_K - 1) / MG_K * MG_K;
   p->vol = (long long)p->n * p->n * p->nb;
   // two-pass coupling for the long transforms unless SLSHT_CUDA_TWO_PASS=0 (the single-pass
@@ -715,9 +715,16 @@ void build_plan(slsht_cuda_plan* p) {
       const int m = p->comps[c0 + i].m;
       int j = i;
       while (j + 1 < ch.count && p->comps[c0 + j + 1].m == m) ++j;
-      p->segs.push_back(Seg{m, p->comps[c0 + i].l, p->comps[c0 + j].l, i});
-      for (int r = i; r <= j; r += MG_ROWS)
-        p->tiles.push_back(MTile{m, r, std::min(MG_ROWS, j - r + 1)});
+      const int l0 = p->comps[c0 + i].l, l1 = p->comps[c0 + j].l;
+      p->segs.push_back(Seg{m, l0, l1, i});
+      // GEMM tiles per parity class of l + m (A rows parity-sorted by k_agen)
+      for (int par = 0; par < 2; ++par) {
+        const int lf = ((l0 + m) & 1) == par ? l0 : l0 + 1;  // first degree of the class
+        if (lf > l1) continue;
+        const int cnt = (l1 - lf) / 2 + 1, arow = i + seg_arow(m, l0, l1, lf);
+        for (int r = 0; r < cnt; r += MG_ROWS)
+          p->tiles.push_back(MTile{m, arow + r, std::min(MG_ROWS, cnt - r), i + (lf - l0) + 2 * r, par});
+      }
       i = j + 1;
     }
     ch.nseg = (int)p->segs.size() - ch.seg0;
@@ -748,9 +755,9 @@ void build_plan(slsht_cuda_plan* p) {
   p->d_weights = dalloc<double>(p->n_nodes);
   p->d_betaw = dalloc<double>(p->nb);
   // node stride ldA (a multiple of the modulated-SHT K chunk), padding zero for the 16-B copies
-  p->d_itab = dalloc<double2>((size_t)(2 * Lf + 1) * p->ldA);
+  p->d_itab = dalloc<double2>((size_t)2 * (2 * Lf + 1) * p->ldA);  // I_0, I_1 rows per order
   p->d_lamh = dalloc<double>((size_t)p->NPQ * p->ldA);
-  CK(cudaMemsetAsync(p->d_itab, 0, sizeof(double2) * (2 * Lf + 1) * p->ldA, s));
+  CK(cudaMemsetAsync(p->d_itab, 0, sizeof(double2) * 2 * (2 * Lf + 1) * p->ldA, s));
   CK(cudaMemsetAsync(p->d_lamh, 0, sizeof(double) * p->NPQ * p->ldA, s));
   size_t dsz = 0;
   for (int pp = 0; pp <= L; ++pp) dsz += (size_t)(2 * pp + 1) * (2 * pp + 1);
@@ -841,6 +848,10 @@ void build_plan(slsht_cuda_plan* p) {
   CK(cudaFuncSetAttribute(k_modgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM));
   if (configure_delta(L) != cudaSuccess)
     throw Status{SLSHT_ERR_VALIDATION, "window band limit too large for the on-chip Delta recursion"};
+  if (4 * sizeof(double) * (p->L_g + 2) > 227 * 1024)
+    throw Status{SLSHT_ERR_VALIDATION, "band limit L_f + L_h too large for the node recursion table"};
+  CK(cudaFuncSetAttribute(k_glnodes, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(4 * sizeof(double) * (p->L_g + 2))));
   for (int c0 = 0; c0 < p->NPQ; c0 += MG_COLS) {  // distinct q per modulated-SHT column tile
     const int c1 = std::min(p->NPQ, c0 + MG_COLS) - 1;
     if (pq[2 * c1] - pq[2 * c0] + 1 > MG_NQ)
@@ -966,13 +977,15 @@ void run_setup(slsht_cuda_plan* p) {
     sp.qoff = p->d_qoff;
     sp.ncos = p->d_ncos;
     sp.nsin = p->d_nsin;
-    sp.weights = p->d_weights;
     sp.betaw = p->d_betaw;
     sp.lamh = p->d_lamh;
     sp.itab = reinterpret_cast<double*>(p->d_itab);
     sp.err = p->d_err;
-    const int nnodes_blocks = (p->n_nodes + L + 1 + 3) / 4;  // 4 warps (weights) per block
+    const int nnodes_blocks = (p->N + 1 + L + 1 + 3) / 4;  // 4 warps (weights) per block
     const size_t sm = sizeof(double) * std::max<size_t>(3 * (L + 1), 5 * (p->L_f + 1) + 1);
+    k_glnodes<<<(p->n_nodes + 63) / 64, 64, 4 * sizeof(double) * (p->L_g + 2), s>>>(
+        p->L_g + 1, p->n_nodes, p->d_ncos, p->d_nsin, p->d_weights);
+    CKL();
     k_setup_main<<<sp.ni + sp.nw + nnodes_blocks, 128, sm, s>>>(sp);
     CKL();
   }
@@ -991,7 +1004,7 @@ void run_setup(slsht_cuda_plan* p) {
   CKL();
   CK(cudaEventRecord(p->ev_wtab, a));
   p->wtab_pending = true;
-  p->launches += 4;
+  p->launches += 5;  // k_glnodes, k_setup_main, k_delta, k_dtab, k_wtab
   record(p, 1);
   accumulate(p, ST_SETUP, 0, 1);
 }
@@ -2242,7 +2255,7 @@ int slsht_cuda_modulated(slsht_cuda_plan* p, const double* f, int count, const i
     std::vector<MTile> tiles;
     for (int i = 0; i < count; ++i) {
       segs.push_back(Seg{m[i], l[i], l[i], i});
-      tiles.push_back(MTile{m[i], i, 1});
+      tiles.push_back(MTile{m[i], i, 1, i, (l[i] + m[i]) & 1});
     }
     if (count <= 0) return;  // nothing requested: an empty result, no launch
     cudaStream_t s = p->stream;
