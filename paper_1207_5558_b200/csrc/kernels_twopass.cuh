@@ -345,7 +345,8 @@ struct QfParams {
   double* partials;      // [comp][tile][8]
   const CompRec* comps;
   int count, n, ncol, ncolp, n_tiles;
-  long long vol;
+  long long vol;  // slot stride of out (complex elements)
+  int rpitch;     // row stride of out: ncol rounded up to whole 128-B lines in the ring
   int mirror;
   const double2* rou;
   const int* perm;
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
       for (int a = a_first; a < N; a += A_STEP, hsh += hstep) {
         const double2 t = Tp[(size_t)perm_s[a] * TS];
         const double vr = t.x, vi = t.y;
-        const size_t idx = (size_t)a * P.ncol;
+        const size_t idx = (size_t)a * P.rpitch;
         __stcs(o + idx, make_double2(vr, vi));
         if constexpr (MIR) {
           const long long br = __double_as_longlong(vr) ^ mflip_r;

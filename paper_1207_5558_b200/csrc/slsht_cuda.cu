@@ -98,6 +98,11 @@ struct slsht_cuda_plan {
   int real_mode = 0, emit_neg = 0, mirror = 0, materialize = 0;
   int MG = 1, NG = 1, n_col_tiles = 0;
   long long vol = 0;            // complex elements per volume
+  // device output layout: row a of a volume at a * rpitch, slots vstride apart. The two-pass
+  // ring pads every row to whole 128-B lines (rpitch = ncol rounded up to 8) so the epilogue
+  // writes aligned lines; elsewhere rpitch = ncol, vstride = vol (the So3Volume layout)
+  int rpitch = 0;
+  long long vstride = 0;
   long long slot_base = 0;      // coeff_index offset of the first materialized slot
   long long n_slots = 0;        // output slots allocated
   long long emitted = 0;
@@ -435,7 +440,9 @@ void build_plan(slsht_cuda_plan* p) {
   for (const auto& c : p->comps) p->emitted += (p->mirror && c.m > 0) ? 2 : 1;
 
   // ---- chunking and output slots
-  const size_t vol_bytes = (size_t)p->vol * 16;
+  p->rpitch = (p->use_tp && !p->materialize) ? (p->ncol + 7) / 8 * 8 : p->ncol;
+  p->vstride = (long long)p->n * p->rpitch;
+  const size_t vol_bytes = (size_t)p->vstride * 16;
   if (p->materialize) {
     p->slot_base = (long long)p->l_begin * p->l_begin;
     p->n_slots = (long long)p->l_end * p->l_end - p->slot_base;
@@ -831,7 +838,7 @@ void build_plan(slsht_cuda_plan* p) {
   if (out_bytes + t_bytes + (64u << 20) > free_b)
     throw Status{SLSHT_ERR_VALIDATION,
                  "device output buffer does not fit in HBM (use the streaming ring mode)"};
-  p->d_out = dalloc<double2>((size_t)p->n_slots * p->vol);
+  p->d_out = dalloc<double2>((size_t)p->n_slots * p->vstride);
   if (p->use_tp) p->d_T = dalloc<double2>(t_bytes / 16);
   const int parts_per_tile = p->use_fused ? FuCfg<49>::EPW : 1;
   p->d_partials = dalloc<double>((size_t)p->max_chunk * p->n_col_tiles * parts_per_tile * 8);
@@ -1193,7 +1200,8 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     qf.ncol = p->ncol;
     qf.ncolp = p->tp_ncolp;
     qf.n_tiles = p->tp_ntiles;
-    qf.vol = p->vol;
+    qf.vol = p->vstride;
+    qf.rpitch = p->rpitch;
     qf.mirror = p->mirror;
     qf.rou = p->d_rou;
     qf.perm = p->d_perm;
@@ -1538,9 +1546,10 @@ void run_capture(slsht_cuda_plan* p, const double* f, const double* h, double* d
       join_fft(p);
       for (const Req& r : reqs)
         if (r.chunk == ci)
-          CK(cudaMemcpyAsync(volumes + 2 * (size_t)(slot ? slot[r.i] : r.i) * p->vol,
-                             p->d_out + (size_t)r.slot * p->vol, (size_t)p->vol * 16,
-                             cudaMemcpyDeviceToHost, p->stream));
+          CK(cudaMemcpy2DAsync(volumes + 2 * (size_t)(slot ? slot[r.i] : r.i) * p->vol,
+                               (size_t)p->ncol * 16, p->d_out + (size_t)r.slot * p->vstride,
+                               (size_t)p->rpitch * 16, (size_t)p->ncol * 16, (size_t)p->n,
+                               cudaMemcpyDeviceToHost, p->stream));
     }
     if (digests) copy_digests(p, digests, false);
     check_numeric(p);
@@ -1567,7 +1576,6 @@ void run_forward_sink(slsht_cuda_plan* p, const double* f, const double* h, slsh
     load_inputs(p, f, h, false);
     run_setup(p);
     check_numeric(p);
-    const size_t vb = (size_t)p->vol * 16;
     auto deliver = [&](size_t ci) {
       const Chunk& ch = p->chunks[ci];
       CK(cudaEventSynchronize(p->ev_copied[ch.buf]));
@@ -1589,13 +1597,16 @@ void run_forward_sink(slsht_cuda_plan* p, const double* f, const double* h, slsh
       CK(cudaEventRecord(p->ev_done[ch.buf], p->stream));
       CK(cudaStreamWaitEvent(p->copy_stream, p->ev_done[ch.buf], 0));
       if (p->fft_last >= 0) CK(cudaStreamWaitEvent(p->copy_stream, p->ev_fft[ch.buf], 0));
-      const double2* src = p->d_out + (size_t)ch.buf * per * p->max_chunk * p->vol;
-      CK(cudaMemcpyAsync(p->h_stage[ch.buf], src, (size_t)ch.count * vb, cudaMemcpyDeviceToHost,
-                         p->copy_stream));
+      // the ring's pitched rows to packed So3Volumes in the host stage
+      const double2* src = p->d_out + (size_t)ch.buf * per * p->max_chunk * p->vstride;
+      const size_t rw = (size_t)p->ncol * 16, sp = (size_t)p->rpitch * 16;
+      const size_t rows = (size_t)ch.count * p->n;
+      CK(cudaMemcpy2DAsync(p->h_stage[ch.buf], rw, src, sp, rw, rows, cudaMemcpyDeviceToHost,
+                           p->copy_stream));
       if (per == 2)
-        CK(cudaMemcpyAsync(p->h_stage[ch.buf] + (size_t)p->max_chunk * p->vol,
-                           src + (size_t)p->max_chunk * p->vol, (size_t)ch.count * vb,
-                           cudaMemcpyDeviceToHost, p->copy_stream));
+        CK(cudaMemcpy2DAsync(p->h_stage[ch.buf] + (size_t)p->max_chunk * p->vol, rw,
+                             src + (size_t)p->max_chunk * p->vstride, sp, rw, rows,
+                             cudaMemcpyDeviceToHost, p->copy_stream));
       CK(cudaEventRecord(p->ev_copied[ch.buf], p->copy_stream));
     }
     const size_t nc = p->chunks.size();
