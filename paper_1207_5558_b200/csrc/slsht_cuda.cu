@@ -134,8 +134,6 @@ struct slsht_cuda_plan {
   bool tp_overlap = false; //   k_qfft + digest of chunk i on fft_stream under k_tgemm of i+1
   bool use_fused = false;  // fused coupling (k_fused, n = 49): GEMM + FFT + epilogue in one
   int fu_KP = 0, fu_upad = 0;
-  signed char* d_kend = nullptr;     // fused: [stage][row group] T row completed, or -1
-  unsigned char* d_kval = nullptr;   // fused: [stage][row group] k-step present
   bool tp_col_fast = false; //  k_tgemm raster: column tiles fastest (W L2-resident)
   bool tp_t_stream = false; //  k_tgemm: T stores with the evict-first hint
   size_t tp_t_elems = 0;   //   one T buffer (two in the overlapped schedule)
@@ -219,8 +217,6 @@ void free_plan(slsht_cuda_plan* p) {
   cudaFree(p->d_f);
   cudaFree(p->d_T);
   cudaFree(p->d_qend);
-  cudaFree(p->d_kend);
-  cudaFree(p->d_kval);
   cudaFree(p->d_wrow);
   cudaFree(p->d_r43);
   cudaFree(p->d_h);
@@ -440,7 +436,7 @@ void build_plan(slsht_cuda_plan* p) {
   for (const auto& c : p->comps) p->emitted += (p->mirror && c.m > 0) ? 2 : 1;
 
   // ---- chunking and output slots
-  p->rpitch = (p->use_tp && !p->materialize) ? (p->ncol + 7) / 8 * 8 : p->ncol;
+  p->rpitch = ((p->use_tp || p->use_fused) && !p->materialize) ? (p->ncol + 7) / 8 * 8 : p->ncol;
   p->vstride = (long long)p->n * p->rpitch;
   const size_t vol_bytes = (size_t)p->vstride * 16;
   if (p->materialize) {
@@ -641,13 +637,9 @@ void build_plan(slsht_cuda_plan* p) {
   // (rows j + G k); each group's sequence of k-steps (its rows in order, every row padded to
   // whole k-steps) is interleaved across the groups: K row ((s G + j) 4 + kl) holds position
   // 4 s + kl of group j's sequence. U (8-component groups, row stride UPAD) and W use it.
-  std::vector<signed char> kend;
-  std::vector<unsigned char> kval;
   if (p->use_fused) {
     using FC = FuCfg<49>;
     wrow.assign(p->NPQ, 0);
-    kend.assign((size_t)FC::NST * FC::G, (signed char)-1);
-    kval.assign((size_t)FC::NST * FC::G, 0);
     for (int j = 0; j < FC::G; ++j) {
       int pos = 0;
       for (int k = 0; k < FC::R1; ++k) {
@@ -661,9 +653,9 @@ void build_plan(slsht_cuda_plan* p) {
           ustr[c] = p->fu_upad;
         }
         pos = (pos + 3) / 4 * 4;
-        kend[(size_t)(pos / 4 - 1) * FC::G + j] = (signed char)r;
+        if (pos / 4 != [&] { int t = 0; for (int e = 0; e <= k; ++e) t += FC::nks(j, e); return t; }())
+          throw Status{SLSHT_ERR_VALIDATION, "internal: fused K layout mismatch"};
       }
-      for (int s0 = 0; s0 < pos / 4; ++s0) kval[(size_t)s0 * FC::G + j] = 1;
       if (pos / 4 > FC::NST)
         throw Status{SLSHT_ERR_VALIDATION, "internal: fused K layout mismatch"};
     }
@@ -777,8 +769,6 @@ void build_plan(slsht_cuda_plan* p) {
     p->d_W = dalloc<double2>(welems);
     CK(cudaMemsetAsync(p->d_W, 0, welems * 16, s));  // padding rows
     p->d_wrow = dupload(wrow, s);
-    p->d_kend = dupload(kend, s);
-    p->d_kval = dupload(kval, s);
   } else if (p->use_tp) {
     p->d_W = dalloc<double2>((size_t)p->tp_KP * p->tp_ncolp);
     CK(cudaMemsetAsync(p->d_W, 0, (size_t)p->tp_KP * p->tp_ncolp * 16, s));  // padding rows
@@ -1068,12 +1058,11 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     fp.n_groups = (ch.count + 7) / 8;
     fp.n_col_tiles = p->n_col_tiles;
     fp.ncol = p->ncol;
-    fp.vol = p->vol;
+    fp.vol = p->vstride;
+    fp.rpitch = p->rpitch;
     fp.mirror = p->mirror;
     fp.rou = p->d_rou;
     fp.betaw = p->d_betaw;
-    fp.kend = p->d_kend;
-    fp.kval = p->d_kval;
     const int grid = std::min(fp.n_groups, p->num_sms);
     k_fused<49><<<grid, FuCfg<49>::NTHREADS, p->couple_smem, s>>>(fp);
   } else if (p->use_lines) {
