@@ -25,7 +25,6 @@
 namespace slsht_cuda {
 
 constexpr int TG_BM = 64;      // components per CTA
-constexpr int TG_BN = 64;      // column padding unit of W and T (the widest CTA tile)
 constexpr int TG_KS = 16;      // (p, q) rows per pipeline stage (4 k-steps)
 constexpr int TG_ASTR = 20;    // A row stride (complex): == 4 mod 8, conflict-free fragments
 // B row stride (complex) BN + 2 == 2 mod 8: conflict-free fragments

@@ -406,7 +406,6 @@ void build_plan(slsht_cuda_plan* p) {
   {
     const char* e = std::getenv("SLSHT_CUDA_TWO_PASS");
     p->use_tp = !(e && e[0] == '0') && tp_kernel(p->n, p->tp_fft, p->tp_threads, p->tp_nt);
-    p->tp_ncolp = (p->ncol + TG_BN - 1) / TG_BN * TG_BN;
     p->tp_ntiles = (p->ncol + p->tp_nt - 1) / p->tp_nt;
     // k_tgemm shape: <32, 2, 2, 3> (three 4-warp CTAs per SM, two stages) unless
     // SLSHT_CUDA_TGEMM selects <64, 2, 4, 1> (0), <32, 2, 3, 2> (1) or <32, 2, 4, 1> (2)
@@ -414,6 +413,8 @@ void build_plan(slsht_cuda_plan* p) {
     p->tp_gv = gv ? std::atoi(gv) : 3;
     if (p->tp_gv < 0 || p->tp_gv > 3) p->tp_gv = 3;
     p->tp_bn = tgemm_variant(p->tp_gv).bn;
+    // T and W column stride: whole GEMM column tiles (a multiple of k_qfft's 32 columns)
+    p->tp_ncolp = (p->ncol + p->tp_bn - 1) / p->tp_bn * p->tp_bn;
   }
   // fused coupling for n = 49 with SLSHT_CUDA_FUSED=1 (opt-in until it beats the two-pass
   // path)
