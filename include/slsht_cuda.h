@@ -77,6 +77,10 @@ typedef struct slsht_cuda_desc {
  * reduced, so every result is bitwise the one-device result. Host-sink calls of the shards are
  * serialized under one mutex, as the reference's worker pool does (transform.cpp:282-284). */
 
+/* Number of visible devices this build can run on (sm_100, B200); 0 when there is none. The
+ * drop-in forward_fast uses all of them by default (one degree shard each). */
+int slsht_cuda_device_count(void);
+
 /* The shard rule of multi-GPU plans (host only, no device needed): bounds[0..parts] of the
  * degree range [l_begin, l_end) for `parts` shards. Returns 0, or SLSHT_ERR_VALIDATION. */
 int slsht_cuda_shard_bounds(int l_begin, int l_end, int real_mode, int parts, int* bounds);

@@ -43,6 +43,7 @@ EXPORTS = [
     "slsht_cuda_forward_direct",
     "slsht_cuda_copy_sink",
     "slsht_cuda_shard_bounds",
+    "slsht_cuda_device_count",
 ]
 
 
@@ -135,5 +136,7 @@ def load() -> C.CDLL:
     lib.slsht_cuda_inverse.restype = C.c_int
     lib.slsht_cuda_shard_bounds.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip]
     lib.slsht_cuda_shard_bounds.restype = C.c_int
+    lib.slsht_cuda_device_count.argtypes = []
+    lib.slsht_cuda_device_count.restype = C.c_int
     _lib = lib
     return lib

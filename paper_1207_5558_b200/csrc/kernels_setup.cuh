@@ -274,8 +274,9 @@ __device__ __forceinline__ size_t delta_offset(int p) {
 //      three-term recursion in m with the values in registers, each value written straight to
 //      all its symmetric positions (transpose with (-1)^(m-m'), then the four quadrants).
 // Explicit _rn intrinsics keep every operation of the reference separately rounded (no FMA
-// contraction), so the table is bit-identical to the reference. One CTA; shared memory
-// (L+1)(L+2) doubles.
+// contraction), so the table is bit-identical to the reference. One CTA; its (L+1)(L+2)
+// doubles of top-row factors and values live in shared memory, or (large L, gws != nullptr)
+// in a global-memory workspace.
 __device__ __forceinline__ int tri_index(int l, int mp) { return l * (l + 1) / 2 + mp; }
 
 __device__ __forceinline__ void delta_put(double* lev, int l, int m, int mp, double v) {
@@ -304,8 +305,10 @@ __device__ __forceinline__ void delta_put(double* lev, int l, int m, int mp, dou
   }
 }
 
-__global__ void __launch_bounds__(1024) k_delta(int L, double* __restrict__ delta) {
-  extern __shared__ double sm[];
+__global__ void __launch_bounds__(1024) k_delta(int L, double* __restrict__ delta,
+                                                double* __restrict__ gws) {
+  extern __shared__ double smem_d[];
+  double* sm = gws ? gws : smem_d;
   const int T = (L + 1) * (L + 2) / 2;
   double* fac = sm;      // [tri(l, mp)] top-row factor of level l
   double* top = sm + T;  // [tri(l, mp)] Delta^l_{l, mp}
@@ -370,17 +373,26 @@ __global__ void __launch_bounds__(1024) k_delta(int L, double* __restrict__ delt
   }
 }
 
-// Shared memory of k_delta for band limit L (the opt-in attribute is set by configure_delta,
-// outside any stream capture).
+// Workspace of k_delta for band limit L: shared memory up to L = 166, above that a global
+// buffer of delta_ws_doubles(L) doubles (delta_needs_gws). The opt-in attribute is set by
+// configure_delta, outside any stream capture.
 inline size_t delta_smem(int L) { return sizeof(double) * (size_t)(L + 1) * (L + 2); }
+inline bool delta_needs_gws(int L) { return delta_smem(L) > 227 * 1024; }
+inline size_t delta_ws_doubles(int L) { return (size_t)(L + 1) * (L + 2); }
 inline cudaError_t configure_delta(int L) {
-  if (delta_smem(L) > 227 * 1024) return cudaErrorInvalidValue;
+  if (delta_needs_gws(L)) return cudaSuccess;
   return cudaFuncSetAttribute(k_delta, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)delta_smem(L));
 }
-// Launch k_delta for band limit L on stream s (one CTA).
-inline cudaError_t launch_delta(int L, double* out, cudaStream_t s) {
-  k_delta<<<1, 1024, delta_smem(L), s>>>(L, out);
+// Launch k_delta for band limit L on stream s (one CTA); gws: the workspace when
+// delta_needs_gws(L).
+inline cudaError_t launch_delta(int L, double* out, cudaStream_t s, double* gws = nullptr) {
+  if (delta_needs_gws(L)) {
+    if (!gws) return cudaErrorInvalidValue;
+    k_delta<<<1, 1024, 0, s>>>(L, out, gws);
+  } else {
+    k_delta<<<1, 1024, delta_smem(L), s>>>(L, out, nullptr);
+  }
   return cudaGetLastError();
 }
 
@@ -436,43 +448,44 @@ __global__ void k_wtab(int L, const double* __restrict__ h, const double* __rest
                        double2* __restrict__ W, int fu_kp = 0) {
   const int n = 2 * L + 1, nb = L + 1, ncol = n * nb;
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  const int c = blockIdx.y;
   const int NPQ = (L + 1) * (L + 1);
   if (col >= ncol_pad) return;
-  // fu_kp > 0: the fused kernel's column-tile-major layout [col / 16][KR][16] with the K row
-  // wrow[c] of the interleaved row-group layout and XOR-swizzled columns (kernels_fused.cuh)
-  auto fused_index = [&](int cl) {
-    const int kr = wrow[c];
-    return ((size_t)(cl / 16) * fu_kp + kr) * 16 + ((cl & 8) | ((cl & 7) ^ ((2 * kr) & 7)));
-  };
-  if (col >= ncol) {
-    W[fu_kp ? fused_index(col)
-            : wrow ? (size_t)wrow[c] * ncol_pad + col : wtile_index(c, col, NPQ, tile_nt)] =
-        make_double2(0.0, 0.0);
-    return;
+  for (int c = blockIdx.y; c < NPQ; c += gridDim.y) {  // gridDim.y <= 65535
+    // fu_kp > 0: the fused kernel's column-tile-major layout [col / 16][KR][16] with the K row
+    // wrow[c] of the interleaved row-group layout and XOR-swizzled columns (kernels_fused.cuh)
+    auto fused_index = [&](int cl) {
+      const int kr = wrow[c];
+      return ((size_t)(cl / 16) * fu_kp + kr) * 16 + ((cl & 8) | ((cl & 7) ^ ((2 * kr) & 7)));
+    };
+    if (col >= ncol) {
+      W[fu_kp ? fused_index(col)
+              : wrow ? (size_t)wrow[c] * ncol_pad + col : wtile_index(c, col, NPQ, tile_nt)] =
+          make_double2(0.0, 0.0);
+      continue;
+    }
+    const int q = pq_q[2 * c], p = pq_q[2 * c + 1];
+    const int b = col / n, cg = col % n;
+    const int w = 2 * p + 1;
+    const double* drow = dtab + delta_offset(p) * nb + (size_t)(q + p) * w * nb + b;
+    double ar = 0.0, ai = 0.0;
+    for (int iqp = 0; iqp < w; ++iqp) {
+      const int qp = iqp - p;
+      const double2 hv = *reinterpret_cast<const double2*>(h + 2 * (p * p + p + qp));
+      const double d = drow[(size_t)iqp * nb];
+      int e = (qp * cg) % n;
+      if (e < 0) e += n;
+      const double2 z = rou[e];
+      const double tr = hv.x * d, ti = hv.y * d;
+      ar += tr * z.x - ti * z.y;
+      ai += tr * z.y + ti * z.x;
+    }
+    // wrow: the two-pass GEMM's q-padded row layout with row stride ncol_pad
+    const size_t dst = fu_kp     ? fused_index(col)
+                       : wrow    ? (size_t)wrow[c] * ncol_pad + col
+                       : tile_nt ? wtile_index(c, col, NPQ, tile_nt)
+                                 : (size_t)c * ncol + col;
+    W[dst] = make_double2(ar, ai);
   }
-  const int q = pq_q[2 * c], p = pq_q[2 * c + 1];
-  const int b = col / n, cg = col % n;
-  const int w = 2 * p + 1;
-  const double* drow = dtab + delta_offset(p) * nb + (size_t)(q + p) * w * nb + b;
-  double ar = 0.0, ai = 0.0;
-  for (int iqp = 0; iqp < w; ++iqp) {
-    const int qp = iqp - p;
-    const double2 hv = *reinterpret_cast<const double2*>(h + 2 * (p * p + p + qp));
-    const double d = drow[(size_t)iqp * nb];
-    int e = (qp * cg) % n;
-    if (e < 0) e += n;
-    const double2 z = rou[e];
-    const double tr = hv.x * d, ti = hv.y * d;
-    ar += tr * z.x - ti * z.y;
-    ai += tr * z.y + ti * z.x;
-  }
-  // wrow: the two-pass GEMM's q-padded row layout with row stride ncol_pad
-  const size_t dst = fu_kp     ? fused_index(col)
-                     : wrow    ? (size_t)wrow[c] * ncol_pad + col
-                     : tile_nt ? wtile_index(c, col, NPQ, tile_nt)
-                               : (size_t)c * ncol + col;
-  W[dst] = make_double2(ar, ai);
 }
 
 

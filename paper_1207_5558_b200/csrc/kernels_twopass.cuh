@@ -351,6 +351,8 @@ struct QfParams {
   const int* perm;
   const double* betaw;
   const double* r43;  // k_r43_table (n = 129)
+  FftPlan fft;        // k_qfft_rt: the runtime DIF plan (radices of n)
+  int generic_dft;    // k_qfft_rt: n has a prime factor without a generated butterfly
 };
 
 // row stride of the k_qfft tile: padded to == 2 (mod 8) for the DMMA radix-43 stage (n = 129)
@@ -480,6 +482,126 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
   if (tid == 0) {
     part[4] = g0r;
     part[5] = g0i;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_qfft_rt: the alpha pass for window band limits without a compile-time kernel and too
+// large for the single-pass runtime kernel's on-chip tile (n > 129, i.e. L_h >= 65 off the
+// BASELINE lengths): one component x NT columns per CTA, the n x NT tile of T in shared
+// memory, the runtime mixed-radix DIF plan of k_couple (fft_runtime), or a dense DFT in the
+// epilogue when n has a prime factor above the generated radices; then the same epilogue
+// (stores, mirror, digest partials per (component, column tile)) as k_couple.
+template <int NT, int NTHR>
+__global__ void __launch_bounds__(NTHR) k_qfft_rt(const QfParams P) {
+  static_assert(NTHR % NT == 0, "threads must cover the columns");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = P.n, L = (n - 1) / 2;
+  double2* Ts = reinterpret_cast<double2*>(smem_raw);
+  double2* rou_s = Ts + (size_t)n * NT;
+  double* betaw_s = reinterpret_cast<double*>(rou_s + n);
+  int* perm_s = reinterpret_cast<int*>(betaw_s + (L + 1));
+  const int tid = threadIdx.x;
+  for (int i = tid; i < n; i += NTHR) {
+    rou_s[i] = P.rou[i];
+    perm_s[i] = P.perm[i];
+  }
+  for (int i = tid; i <= L; i += NTHR) betaw_s[i] = P.betaw[i];
+  const int ct = blockIdx.x, comp = blockIdx.y;
+  const int col0 = ct * NT;
+  {
+    const double2* src = P.T + (size_t)comp * n * P.ncolp + col0;
+    for (int e = tid; e < n * NT; e += NTHR) {
+      const int row = e / NT, c = e % NT;
+      cp_async16(Ts + (size_t)row * NT + c, src + (size_t)row * P.ncolp + c, true);
+    }
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  if (!P.generic_dft) fft_runtime(Ts, NT, n, NT, P.fft, rou_s, NTHR);
+
+  const int cc = tid % NT, col = col0 + cc;
+  const bool ok = col < P.ncol;
+  double s2 = 0.0, pr = 0.0, pi = 0.0, ir = 0.0, ii = 0.0, g0r = 0.0, g0i = 0.0;
+  long long mx2 = 0;
+  if (ok) {
+    const CompRec rec = P.comps[comp];
+    double2* o = P.out + rec.slot * P.vol + col;
+    double2* om = (P.mirror && rec.m > 0) ? P.out + rec.mslot * P.vol + col : nullptr;
+    const long long sbit = (long long)0x8000000000000000ULL;
+    const long long mflip_r = (rec.m & 1) ? sbit : 0, mflip_i = (rec.m & 1) ? 0 : sbit;
+    const double qb = betaw_s[col / n];
+    const double2* Tp = Ts + cc;
+    const int a_first = tid / NT;
+    constexpr int A_STEP = NTHR / NT;
+    uint32_t hsh = (uint32_t)((size_t)a_first * P.ncol + col) * 0x9E3779B1u;
+    const uint32_t hstep = (uint32_t)((size_t)A_STEP * P.ncol) * 0x9E3779B1u;
+    for (int a = a_first; a < n; a += A_STEP, hsh += hstep) {
+      double vr, vi;
+      if (!P.generic_dft) {
+        const double2 t = Tp[(size_t)perm_s[a] * NT];
+        vr = t.x;
+        vi = t.y;
+      } else {  // dense DFT: g_a = sum_j w^(j a) T_j
+        double sr = 0.0, si = 0.0;
+        int e = 0;
+        for (int j = 0; j < n; ++j) {
+          const double2 t = Tp[(size_t)j * NT];
+          const double2 w = rou_s[e];
+          sr += t.x * w.x - t.y * w.y;
+          si += t.x * w.y + t.y * w.x;
+          e += a;
+          if (e >= n) e -= n;
+        }
+        vr = sr;
+        vi = si;
+      }
+      const size_t idx = (size_t)a * P.rpitch;
+      __stcs(o + idx, make_double2(vr, vi));
+      if (om) {
+        const long long br = __double_as_longlong(vr) ^ mflip_r;
+        const long long bi = __double_as_longlong(vi) ^ mflip_i;
+        __stcs(om + idx, make_double2(__longlong_as_double(br), __longlong_as_double(bi)));
+      }
+      const double a2 = fma(vr, vr, vi * vi);
+      s2 += a2;
+      mx2 = max(mx2, __double_as_longlong(a2));
+      const double wgt = digest_weight(hsh);
+      pr = fma(wgt, vr, pr);
+      pi = fma(wgt, vi, pi);
+      ir += vr;
+      ii += vi;
+      if (a == 0 && col == 0) {
+        g0r = vr;
+        g0i = vi;
+      }
+    }
+    ir *= qb;
+    ii *= qb;
+  }
+  // fixed-order reduction: a shuffle tree per warp, then the warps in order
+  double v[8] = {s2, __longlong_as_double(mx2), pr, pi, g0r, g0i, ir, ii};
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double x = __shfl_down_sync(0xffffffffu, v[k], off);
+      v[k] = (k == 1) ? fmax(v[k], x) : v[k] + x;
+    }
+  __syncthreads();  // T is reused as the reduction scratch
+  double* red = reinterpret_cast<double*>(smem_raw);
+  if ((tid & 31) == 0)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) red[(tid >> 5) * 8 + k] = v[k];
+  __syncthreads();
+  if (tid < 8) {
+    double acc = 0.0;
+    for (int w = 0; w < NTHR / 32; ++w) {
+      const double x = red[w * 8 + tid];
+      acc = (tid == 1) ? fmax(acc, x) : acc + x;
+    }
+    P.partials[((size_t)comp * P.n_tiles + ct) * 8 + tid] = acc;
   }
 }
 

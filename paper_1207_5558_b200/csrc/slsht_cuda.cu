@@ -153,6 +153,7 @@ struct slsht_cuda_plan {
   long long graph_launches = 0;
   bool own_stream = false;
   bool profile = false;
+  bool built = false;  // build_plan completed (single-device plans)
   std::string last_error;
   long long launches = 0;
   double stage_ms[ST_COUNT] = {0, 0, 0, 0, 0, 0};
@@ -168,6 +169,7 @@ struct slsht_cuda_plan {
   double2* d_itab = nullptr;
   double* d_lamh = nullptr;
   double* d_delta = nullptr;
+  double* d_delta_ws = nullptr;  // k_delta workspace for large window band limits
   double* d_dtab = nullptr;
   double2* d_W = nullptr;
   double2* d_rou = nullptr;
@@ -227,6 +229,7 @@ void free_plan(slsht_cuda_plan* p) {
   cudaFree(p->d_itab);
   cudaFree(p->d_lamh);
   cudaFree(p->d_delta);
+  cudaFree(p->d_delta_ws);
   cudaFree(p->d_dtab);
   cudaFree(p->d_W);
   cudaFree(p->d_rou);
@@ -360,7 +363,13 @@ bool tp_kernel(int n, void (*&fn)(QfParams), int& threads, int& nt) {
     case 49: fn = k_qfft<49, 32, 128, 6>; break;
     case 65: fn = k_qfft<65, 32, 128, 5>; break;
     case 129: fn = k_qfft<129, 32, 128, 3>; break;  // radix-43 stage on DMMA: 168 registers
-    default: return false;
+    default:
+      // longer transforms (n > 129) without a compile-time kernel: the runtime-plan alpha pass
+      // (8 columns per CTA: the n x 8 tile of T fits in shared memory up to n ~ 1500)
+      if (n <= 129) return false;
+      fn = k_qfft_rt<8, 128>;
+      nt = 8;
+      break;
   }
   return true;
 }
@@ -374,6 +383,31 @@ int couple_threads(int n) {
   }
 }
 
+// The dynamic shared-memory opt-in of this plan's kernels. The attribute belongs to the kernel
+// function, not to the plan, and several plans can share a kernel with different sizes (the
+// runtime-length kernels), so it is applied again at every entry point (cheap host calls,
+// outside any stream capture) as well as at build time.
+void set_func_attributes(const slsht_cuda_plan* p) {
+  auto opt = [](auto fn, size_t bytes) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  };
+  opt(k_modgemm, MG_SMEM);
+  CK(configure_delta(p->L_h));
+  opt(k_glnodes, 4 * sizeof(double) * (p->L_g + 2));
+  if (p->use_fused) {
+    opt(k_fused<49>, p->couple_smem);
+  } else if (p->use_lines) {
+    opt(p->lines_fn, p->couple_smem);
+  } else if (p->use_tp) {
+    opt(tgemm_variant(p->tp_gv).fn, p->tp_gemm_smem);
+    opt(p->tp_fft, p->tp_fft_smem);
+  } else if (p->use_ws) {
+    opt(p->ws.fn, p->couple_smem);
+  } else {
+    opt(couple_kernel(p->n, p->MG, p->NG), p->couple_smem);
+  }
+}
+
 void build_plan(slsht_cuda_plan* p) {
   const slsht_cuda_desc& d = p->desc;
   if (d.L_f < 0 || d.L_h < 0) throw Status{SLSHT_ERR_VALIDATION, "band limit must be non-negative"};
@@ -383,8 +417,6 @@ void build_plan(slsht_cuda_plan* p) {
   p->lmax = d.lmax < 0 ? p->L_g : d.lmax;
   if (p->lmax > p->L_g)
     throw Status{SLSHT_ERR_VALIDATION, "fast engine computes components up to L_f + L_h only"};
-  if (2 * d.L_h + 1 > 221)
-    throw Status{SLSHT_ERR_VALIDATION, "window band limit above 110 is not supported by this build"};
   p->l_begin = std::max(0, d.l_begin);
   p->l_end = d.l_end < 0 ? p->lmax + 1 : std::min(d.l_end, p->lmax + 1);
   if (p->l_begin > p->l_end) throw Status{SLSHT_ERR_VALIDATION, "empty or inverted degree range"};
@@ -761,7 +793,25 @@ void build_plan(slsht_cuda_plan* p) {
   CK(cudaMemsetAsync(p->d_lamh, 0, sizeof(double) * p->NPQ * p->ldA, s));
   size_t dsz = 0;
   for (int pp = 0; pp <= L; ++pp) dsz += (size_t)(2 * pp + 1) * (2 * pp + 1);
+  {
+    // the window tables grow as L_h^4 (d(beta): sum (2p+1)^2 (L_h+1) doubles, W: ~(L_h+1)^2 x
+    // n (L_h+1) complex); say so before allocating them
+    const size_t wbytes = (size_t)(p->use_tp ? p->tp_KP : p->NPQ) *
+                          (size_t)(p->use_tp ? p->tp_ncolp : p->ncol + 64) * 16;
+    const size_t need = dsz * p->nb * 8 + wbytes;
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    if (need + (256u << 20) > free_b) {
+      char msg[200];
+      std::snprintf(msg, sizeof msg,
+                    "window band limit %d: the window tables need %.1f GB of device memory, "
+                    "%.1f GB are free",
+                    L, need / 1e9, free_b / 1e9);
+      throw Status{SLSHT_ERR_DEVICE, msg};
+    }
+  }
   p->d_delta = dalloc<double>(dsz);
+  if (delta_needs_gws(L)) p->d_delta_ws = dalloc<double>(delta_ws_doubles(L));
   p->d_dtab = dalloc<double>(dsz * p->nb);
   const int tile_nt_alloc = p->use_lines ? 8 : (p->use_ws ? p->ws.NT : 0);
   const size_t ncol_pad = tile_nt_alloc ? (size_t)p->n_col_tiles * tile_nt_alloc : (size_t)p->ncol;
@@ -843,13 +893,8 @@ void build_plan(slsht_cuda_plan* p) {
   for (auto& e : p->ev_lazy) CK(cudaEventCreate(&e));
 
   p->num_sms = prop.multiProcessorCount;
-  CK(cudaFuncSetAttribute(k_modgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM));
-  if (configure_delta(L) != cudaSuccess)
-    throw Status{SLSHT_ERR_VALIDATION, "window band limit too large for the on-chip Delta recursion"};
   if (4 * sizeof(double) * (p->L_g + 2) > 227 * 1024)
     throw Status{SLSHT_ERR_VALIDATION, "band limit L_f + L_h too large for the node recursion table"};
-  CK(cudaFuncSetAttribute(k_glnodes, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)(4 * sizeof(double) * (p->L_g + 2))));
   for (int c0 = 0; c0 < p->NPQ; c0 += MG_COLS) {  // distinct q per modulated-SHT column tile
     const int c1 = std::min(p->NPQ, c0 + MG_COLS) - 1;
     if (pq[2 * c1] - pq[2 * c0] + 1 > MG_NQ)
@@ -857,18 +902,12 @@ void build_plan(slsht_cuda_plan* p) {
   }
   if (p->use_fused) {
     p->couple_smem = FuCfg<49>::SMEM;
-    CK(cudaFuncSetAttribute(k_fused<49>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)p->couple_smem));
   } else if (p->use_lines) {
-    CK(cudaFuncSetAttribute(p->lines_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)p->couple_smem));
   } else if (p->use_tp) {
     p->tp_gemm_smem = tgemm_smem_bytes(p->tp_KP, p->tp_bn, tgemm_variant(p->tp_gv).nst,
                                        tgemm_variant(p->tp_gv).bm);
     p->tp_fft_smem = qfft_smem_bytes(p->n, p->tp_nt);
     p->couple_smem = std::max(p->tp_gemm_smem, p->tp_fft_smem);
-    CK(cudaFuncSetAttribute(tgemm_variant(p->tp_gv).fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)p->tp_gemm_smem));
     if (p->tp_overlap) {
       CK(cudaStreamCreateWithFlags(&p->fft_stream, cudaStreamNonBlocking));
       for (int i = 0; i < 2; ++i) {
@@ -876,16 +915,10 @@ void build_plan(slsht_cuda_plan* p) {
         CK(cudaEventCreateWithFlags(&p->ev_fft[i], cudaEventDisableTiming));
       }
     }
-    CK(cudaFuncSetAttribute(p->tp_fft, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)p->tp_fft_smem));
   } else if (p->use_ws) {
     p->couple_smem = p->ws.smem;
-    CK(cudaFuncSetAttribute(p->ws.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)p->couple_smem));
   } else {
     p->couple_smem = couple_smem_bytes(p->n, p->MG, p->NG);
-    CK(cudaFuncSetAttribute(couple_kernel(p->n, p->MG, p->NG),
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->couple_smem));
   }
   if (p->use_lines) {
     // execution split: the divisor of the digest split with the best balance over the SMs for
@@ -909,6 +942,8 @@ void build_plan(slsht_cuda_plan* p) {
   }
   if (p->couple_smem > (size_t)prop.sharedMemPerBlockOptin)
     throw Status{SLSHT_ERR_VALIDATION, "window band limit too large for the shared-memory tile"};
+  set_func_attributes(p);
+  p->built = true;
   CK(cudaStreamSynchronize(s));
 }
 
@@ -988,7 +1023,7 @@ void run_setup(slsht_cuda_plan* p) {
     CKL();
   }
   cudaStream_t a = p->aux_stream;
-  CK(launch_delta(L, p->d_delta, a));
+  CK(launch_delta(L, p->d_delta, a, p->d_delta_ws));
   const int wmax = (2 * L + 1) * (2 * L + 1) * p->nb;
   k_dtab<<<dim3((wmax + 255) / 256, L + 1), 256, 0, a>>>(L, p->d_delta, p->d_rou, p->d_dtab);
   CKL();
@@ -996,7 +1031,7 @@ void run_setup(slsht_cuda_plan* p) {
   const int ncol_pad = p->use_fused ? p->n_col_tiles * FuCfg<49>::NT
                        : p->use_tp  ? p->tp_ncolp
                                     : (tile_nt ? p->n_col_tiles * tile_nt : p->ncol);
-  k_wtab<<<dim3((ncol_pad + 127) / 128, p->NPQ), 128, 0, a>>>(
+  k_wtab<<<dim3((ncol_pad + 127) / 128, std::min(p->NPQ, 65535)), 128, 0, a>>>(
       L, p->d_h, p->d_dtab, p->d_rou, p->d_pq, tile_nt, ncol_pad,
       (p->use_tp || p->use_fused) ? p->d_wrow : nullptr, p->d_W, p->use_fused ? p->fu_KP : 0);
   CKL();
@@ -1197,6 +1232,8 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     qf.perm = p->d_perm;
     qf.betaw = p->d_betaw;
     qf.r43 = p->d_r43;
+    qf.fft = p->fft;
+    qf.generic_dft = p->generic_dft;
     p->tp_fft<<<dim3(p->tp_ntiles, ch.count), p->tp_threads, p->tp_fft_smem, fs>>>(qf);
     CKL();
     if (overlap) {
@@ -1268,6 +1305,7 @@ template <class F>
 int guarded(slsht_cuda_plan* p, F&& fn) {
   try {
     if (p) CK(cudaSetDevice(p->desc.device));
+    if (p && p->parts.empty() && p->built) set_func_attributes(p);
     fn();
     return SLSHT_OK;
   } catch (const Status& st) {
@@ -1728,6 +1766,19 @@ int slsht_cuda_stage_times(const slsht_cuda_plan* p, double* out_ms, int n) {
   return k;
 }
 
+int slsht_cuda_device_count(void) {
+  int n = 0, usable = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  for (int d = 0; d < n; ++d) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && prop.major == 10) ++usable;
+  }
+  return usable;
+}
+
 int slsht_cuda_shard_bounds(int l_begin, int l_end, int real_mode, int parts, int* bounds) {
   if (parts < 1 || !bounds || l_begin < 0 || l_end < l_begin) return SLSHT_ERR_VALIDATION;
   const std::vector<int> b = shard_bounds(l_begin, l_end, real_mode != 0, parts);
@@ -1981,8 +2032,6 @@ int slsht_cuda_forward_direct(int device, int L_f, const double* f, int L_h, con
   try {
     if (L_f < 0 || L_h < 0) throw Status{SLSHT_ERR_VALIDATION, "band limit must be non-negative"};
     if (!f || !h || !out) throw Status{SLSHT_ERR_VALIDATION, "null argument"};
-    if (2 * L_h + 1 > 221)
-      throw Status{SLSHT_ERR_VALIDATION, "window band limit above 110 is not supported by this build"};
     const int L_g = L_f + L_h;
     if (lmax < 0) lmax = L_g;
     const int L = std::max(lmax, L_g);  // sphere-grid band (transform.cpp:319)
@@ -2040,13 +2089,13 @@ int slsht_cuda_forward_direct(int device, int L_f, const double* f, int L_h, con
     double* d_delta = (double*)dal(8 * dsz);
     double* d_dtab = (double*)dal(8 * dsz * nb);
     double2* d_W = (double2*)dal(16 * (size_t)NPQ * ncol);
-    if (configure_delta(L_h) != cudaSuccess)
-      throw Status{SLSHT_ERR_VALIDATION, "window band limit too large for the on-chip Delta recursion"};
-    CK(launch_delta(L_h, d_delta, s));
+    CK(configure_delta(L_h));
+    double* d_dws = delta_needs_gws(L_h) ? (double*)dal(8 * delta_ws_doubles(L_h)) : nullptr;
+    CK(launch_delta(L_h, d_delta, s, d_dws));
     const int wmax = nh * nh * nb;
     k_dtab<<<dim3(blocks(wmax, 256), L_h + 1), 256, 0, s>>>(L_h, d_delta, d_rou, d_dtab);
     CKL();
-    k_wtab<<<dim3(blocks(ncol, 128), NPQ), 128, 0, s>>>(L_h, d_h, d_dtab, d_rou, d_pq, 0, ncol,
+    k_wtab<<<dim3(blocks(ncol, 128), std::min(NPQ, 65535)), 128, 0, s>>>(L_h, d_h, d_dtab, d_rou, d_pq, 0, ncol,
                                                        nullptr, d_W);
     CKL();
     // ---- synthesis tables: lambda_p^q(theta_t) in q-major (p,q) rows; F = sh_synthesis(f)
@@ -2177,17 +2226,15 @@ int slsht_cuda_delta_tables(int device, int L, double* out) {
   try {
     if (L < 0) throw Status{SLSHT_ERR_VALIDATION, "band limit must be non-negative"};
     if (!out) throw Status{SLSHT_ERR_VALIDATION, "null output"};
-    if (delta_smem(L) > 227 * 1024)  // checked before any allocation
-      throw Status{SLSHT_ERR_VALIDATION, "band limit too large for the on-chip Delta recursion"};
     int dev_count = 0;
     if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
       throw Status{SLSHT_ERR_DEVICE, "no CUDA device available (the engine has no CPU fallback)"};
     CK(cudaSetDevice(device));
     size_t dsz = 0;
     for (int pp = 0; pp <= L; ++pp) dsz += (size_t)(2 * pp + 1) * (2 * pp + 1);
-    d = dalloc<double>(dsz);
+    d = dalloc<double>(dsz + (delta_needs_gws(L) ? delta_ws_doubles(L) : 0));
     CK(configure_delta(L));
-    CK(launch_delta(L, d, 0));
+    CK(launch_delta(L, d, 0, delta_needs_gws(L) ? d + dsz : nullptr));
     CK(cudaMemcpy(out, d, dsz * sizeof(double), cudaMemcpyDeviceToHost));
     CK(cudaFree(d));
     return SLSHT_OK;

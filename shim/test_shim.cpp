@@ -13,7 +13,9 @@
 //    io::DistributionWriter as the sink, read back with io::read_component (SURVEY 8(f)
 //    next-2: host sink delivery and on-disk format through the drop-in).
 // Prints one PASS/FAIL line per check; exit status 0 iff all pass.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <complex>
 #include <cstdio>
 #include <map>
@@ -216,6 +218,27 @@ int main() {
     }
     report(threw, "eigenfunction_window: theta_c > a throws ValidationError", threw ? 0.0 : 1.0,
            0.0);
+  }
+  {
+    // the shim's plan cache: repeated calls (same and interleaved shapes, with a validation
+    // error in between) give bitwise the results of fresh plans
+    const SphCoeffs f = random_complex(10, 61), h = random_complex(4, 62);
+    const SphCoeffs f2 = random_complex(7, 63), h2 = random_complex(3, 64);
+    const SlshtDistribution a1 = forward_fast(f, h);
+    const SlshtDistribution b1 = forward_fast(f2, h2);
+    ForwardOptions bad;
+    bad.lmax = 99;
+    try {
+      forward_fast(f, h, bad);
+    } catch (const ValidationError&) {
+    }
+    const SlshtDistribution a2 = forward_fast(f, h);
+    const SlshtDistribution b2 = forward_fast(f2, h2);
+    setenv("SLSHT_CUDA_PLAN_CACHE", "0", 1);
+    const SlshtDistribution a3 = forward_fast(f, h);
+    unsetenv("SLSHT_CUDA_PLAN_CACHE");
+    const double d = std::max({max_diff(a1, a2), max_diff(b1, b2), max_diff(a1, a3)});
+    report(d == 0.0, "plan cache: repeated calls bitwise equal to fresh plans", d, 0.0);
   }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ALL PASSED", failures);
   return failures ? 1 : 0;
