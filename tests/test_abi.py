@@ -74,9 +74,8 @@ def test_validation_precedes_device_checks():
     h = S.SphCoeffs(1, np.zeros(4))
     with pytest.raises(S.ValidationError):
         S.forward_fast(f, h, opts=S.ForwardOptions(lmax=5))
-    with pytest.raises(S.ValidationError):  # band limits are checked before the device
-        S.forward_direct(S.SphCoeffs(2, np.zeros(9)), S.SphCoeffs(111, np.zeros(112 * 112)),
-                         cells=[0])
+    with pytest.raises(S.ValidationError):  # arguments are checked before the device
+        S.forward_direct(S.SphCoeffs(2, np.zeros(9)), S.SphCoeffs(3, np.zeros(16)), cells=[])
 
 
 @pytest.mark.skipif(_cuda_available(), reason="checks the no-GPU error path")
