@@ -70,6 +70,13 @@ T* dupload(const std::vector<T>& v, cudaStream_t s) {
   return p;
 }
 
+constexpr size_t kGuardBytes = 65536;
+
+template <class T>
+T* palloc(slsht_cuda_plan* p, size_t count);
+void pfree(slsht_cuda_plan* p, void* ptr);
+void check_guards(slsht_cuda_plan* p);
+
 struct Chunk {
   long long comp0;
   int count;
@@ -154,6 +161,16 @@ struct slsht_cuda_plan {
   bool own_stream = false;
   bool profile = false;
   bool built = false;  // build_plan completed (single-device plans)
+  // SLSHT_CUDA_GUARD=1: every plan-owned device buffer is allocated with 64-KB guard bands on
+  // both sides (pattern 0xA5), checked after every call (bounds checking of global memory; the
+  // pool has no compute-sanitizer)
+  struct GuardedBuf {
+    void* user;
+    char* base;
+    size_t bytes;
+  };
+  bool guard = false;
+  std::vector<GuardedBuf> guards;
   std::string last_error;
   long long launches = 0;
   double stage_ms[ST_COUNT] = {0, 0, 0, 0, 0, 0};
@@ -209,6 +226,53 @@ struct slsht_cuda_plan {
 
 namespace {
 
+template <class T>
+T* palloc(slsht_cuda_plan* p, size_t count) {
+  if (!p->guard) return dalloc<T>(count);
+  if (count == 0) count = 1;
+  const size_t bytes = count * sizeof(T);
+  char* base = nullptr;
+  CK(cudaMalloc(&base, bytes + 2 * kGuardBytes));
+  CK(cudaMemset(base, 0xA5, kGuardBytes));
+  CK(cudaMemset(base + kGuardBytes + bytes, 0xA5, kGuardBytes));
+  p->guards.push_back({base + kGuardBytes, base, bytes});
+  return reinterpret_cast<T*>(base + kGuardBytes);
+}
+
+void pfree(slsht_cuda_plan* p, void* ptr) {
+  if (!ptr) return;
+  for (auto& g : p->guards)
+    if (g.user == ptr) {
+      cudaFree(g.base);
+      g.user = nullptr;
+      return;
+    }
+  cudaFree(ptr);
+}
+
+// Every guard band still holds its pattern (after the device is idle).
+void check_guards(slsht_cuda_plan* p) {
+  if (!p->guard) return;
+  CK(cudaDeviceSynchronize());
+  std::vector<unsigned char> band(kGuardBytes);
+  for (size_t i = 0; i < p->guards.size(); ++i) {
+    const auto& g = p->guards[i];
+    if (!g.user) continue;
+    for (int side = 0; side < 2; ++side) {
+      const char* src = side ? g.base + kGuardBytes + g.bytes : g.base;
+      CK(cudaMemcpy(band.data(), src, kGuardBytes, cudaMemcpyDeviceToHost));
+      for (size_t k = 0; k < kGuardBytes; ++k)
+        if (band[k] != 0xA5) {
+          char msg[160];
+          std::snprintf(msg, sizeof msg,
+                        "guard band %s device buffer #%zu (%zu bytes) overwritten at byte %zu",
+                        side ? "after" : "before", i, g.bytes, k);
+          throw Status{SLSHT_ERR_DEVICE, msg};
+        }
+    }
+  }
+}
+
 void free_plan(slsht_cuda_plan* p) {
   if (!p) return;
   for (slsht_cuda_plan* q : p->parts) {
@@ -216,38 +280,38 @@ void free_plan(slsht_cuda_plan* p) {
     free_plan(q);
   }
   p->parts.clear();
-  cudaFree(p->d_f);
-  cudaFree(p->d_T);
-  cudaFree(p->d_qend);
-  cudaFree(p->d_wrow);
-  cudaFree(p->d_r43);
-  cudaFree(p->d_h);
-  cudaFree(p->d_ncos);
-  cudaFree(p->d_nsin);
-  cudaFree(p->d_weights);
-  cudaFree(p->d_betaw);
-  cudaFree(p->d_itab);
-  cudaFree(p->d_lamh);
-  cudaFree(p->d_delta);
-  cudaFree(p->d_delta_ws);
-  cudaFree(p->d_dtab);
-  cudaFree(p->d_W);
-  cudaFree(p->d_rou);
-  cudaFree(p->d_phase);
-  cudaFree(p->d_perm);
-  cudaFree(p->d_qoff);
-  cudaFree(p->d_pq);
-  cudaFree(p->d_ubase);
-  cudaFree(p->d_ustr);
-  cudaFree(p->d_err);
-  cudaFree(p->d_comps);
-  cudaFree(p->d_segs);
-  cudaFree(p->d_tiles);
-  cudaFree(p->d_A);
-  cudaFree(p->d_U);
-  cudaFree(p->d_out);
-  cudaFree(p->d_partials);
-  cudaFree(p->d_digest);
+  pfree(p, p->d_f);
+  pfree(p, p->d_T);
+  pfree(p, p->d_qend);
+  pfree(p, p->d_wrow);
+  pfree(p, p->d_r43);
+  pfree(p, p->d_h);
+  pfree(p, p->d_ncos);
+  pfree(p, p->d_nsin);
+  pfree(p, p->d_weights);
+  pfree(p, p->d_betaw);
+  pfree(p, p->d_itab);
+  pfree(p, p->d_lamh);
+  pfree(p, p->d_delta);
+  pfree(p, p->d_delta_ws);
+  pfree(p, p->d_dtab);
+  pfree(p, p->d_W);
+  pfree(p, p->d_rou);
+  pfree(p, p->d_phase);
+  pfree(p, p->d_perm);
+  pfree(p, p->d_qoff);
+  pfree(p, p->d_pq);
+  pfree(p, p->d_ubase);
+  pfree(p, p->d_ustr);
+  pfree(p, p->d_err);
+  pfree(p, p->d_comps);
+  pfree(p, p->d_segs);
+  pfree(p, p->d_tiles);
+  pfree(p, p->d_A);
+  pfree(p, p->d_U);
+  pfree(p, p->d_out);
+  pfree(p, p->d_partials);
+  pfree(p, p->d_digest);
   for (int i = 0; i < 2; ++i) {
     if (p->h_stage[i]) cudaFreeHost(p->h_stage[i]);
     if (p->ev_done[i]) cudaEventDestroy(p->ev_done[i]);
@@ -411,6 +475,10 @@ void set_func_attributes(const slsht_cuda_plan* p) {
 void build_plan(slsht_cuda_plan* p) {
   const slsht_cuda_desc& d = p->desc;
   if (d.L_f < 0 || d.L_h < 0) throw Status{SLSHT_ERR_VALIDATION, "band limit must be non-negative"};
+  {
+    const char* g = std::getenv("SLSHT_CUDA_GUARD");
+    p->guard = g && g[0] == '1';
+  }
   p->L_f = d.L_f;
   p->L_h = d.L_h;
   p->L_g = d.L_f + d.L_h;
@@ -778,17 +846,17 @@ void build_plan(slsht_cuda_plan* p) {
 
   // ---- device memory
   const int Lf = p->L_f;
-  p->d_f = dalloc<double>(2 * coeff_count(Lf));
-  p->d_h = dalloc<double>(2 * coeff_count(L));
+  p->d_f = palloc<double>(p, 2 * coeff_count(Lf));
+  p->d_h = palloc<double>(p, 2 * coeff_count(L));
   CK(cudaMemsetAsync(p->d_h, 0, sizeof(double) * 2 * coeff_count(L), s));
   CK(cudaMemsetAsync(p->d_f, 0, sizeof(double) * 2 * coeff_count(Lf), s));
-  p->d_ncos = dalloc<double>(p->n_nodes);
-  p->d_nsin = dalloc<double>(p->n_nodes);
-  p->d_weights = dalloc<double>(p->n_nodes);
-  p->d_betaw = dalloc<double>(p->nb);
+  p->d_ncos = palloc<double>(p, p->n_nodes);
+  p->d_nsin = palloc<double>(p, p->n_nodes);
+  p->d_weights = palloc<double>(p, p->n_nodes);
+  p->d_betaw = palloc<double>(p, p->nb);
   // node stride ldA (a multiple of the modulated-SHT K chunk), padding zero for the 16-B copies
-  p->d_itab = dalloc<double2>((size_t)2 * (2 * Lf + 1) * p->ldA);  // I_0, I_1 rows per order
-  p->d_lamh = dalloc<double>((size_t)p->NPQ * p->ldA);
+  p->d_itab = palloc<double2>(p, (size_t)2 * (2 * Lf + 1) * p->ldA);  // I_0, I_1 rows per order
+  p->d_lamh = palloc<double>(p, (size_t)p->NPQ * p->ldA);
   CK(cudaMemsetAsync(p->d_itab, 0, sizeof(double2) * 2 * (2 * Lf + 1) * p->ldA, s));
   CK(cudaMemsetAsync(p->d_lamh, 0, sizeof(double) * p->NPQ * p->ldA, s));
   size_t dsz = 0;
@@ -810,28 +878,28 @@ void build_plan(slsht_cuda_plan* p) {
       throw Status{SLSHT_ERR_DEVICE, msg};
     }
   }
-  p->d_delta = dalloc<double>(dsz);
-  if (delta_needs_gws(L)) p->d_delta_ws = dalloc<double>(delta_ws_doubles(L));
-  p->d_dtab = dalloc<double>(dsz * p->nb);
+  p->d_delta = palloc<double>(p, dsz);
+  if (delta_needs_gws(L)) p->d_delta_ws = palloc<double>(p, delta_ws_doubles(L));
+  p->d_dtab = palloc<double>(p, dsz * p->nb);
   const int tile_nt_alloc = p->use_lines ? 8 : (p->use_ws ? p->ws.NT : 0);
   const size_t ncol_pad = tile_nt_alloc ? (size_t)p->n_col_tiles * tile_nt_alloc : (size_t)p->ncol;
   if (p->use_fused) {
     const size_t welems = (size_t)p->n_col_tiles * p->fu_KP * FuCfg<49>::NT;
-    p->d_W = dalloc<double2>(welems);
+    p->d_W = palloc<double2>(p, welems);
     CK(cudaMemsetAsync(p->d_W, 0, welems * 16, s));  // padding rows
     p->d_wrow = dupload(wrow, s);
   } else if (p->use_tp) {
-    p->d_W = dalloc<double2>((size_t)p->tp_KP * p->tp_ncolp);
+    p->d_W = palloc<double2>(p, (size_t)p->tp_KP * p->tp_ncolp);
     CK(cudaMemsetAsync(p->d_W, 0, (size_t)p->tp_KP * p->tp_ncolp * 16, s));  // padding rows
     p->d_wrow = dupload(wrow, s);
     p->d_qend = dupload(qend, s);
     if (p->n == 129) {
-      p->d_r43 = dalloc<double>(2 * 576);
+      p->d_r43 = palloc<double>(p, 2 * 576);
       k_r43_table<<<3, 192, 0, s>>>(p->d_r43);
       CKL();
     }
   } else {
-    p->d_W = dalloc<double2>((size_t)p->NPQ * ncol_pad);
+    p->d_W = palloc<double2>(p, (size_t)p->NPQ * ncol_pad);
   }
   p->ct_fast = (size_t)p->NPQ * ncol_pad * 16 < (48u << 20);
   p->d_ubase = dupload(ubase, s);
@@ -841,26 +909,26 @@ void build_plan(slsht_cuda_plan* p) {
   p->d_perm = dupload(perm, s);
   p->d_qoff = dupload(qoff, s);
   p->d_pq = dupload(pq, s);
-  p->d_err = dalloc<int>(1);
+  p->d_err = palloc<int>(p, 1);
   CK(cudaMemsetAsync(p->d_err, 0, sizeof(int), s));
   p->d_comps = dupload(p->comps, s);
   p->d_segs = dupload(p->segs, s);
   p->d_tiles = dupload(p->tiles, s);
-  p->d_A = dalloc<double>((size_t)p->max_chunk * p->ldA);
+  p->d_A = palloc<double>(p, (size_t)p->max_chunk * p->ldA);
   if (p->use_fused) {
     const size_t uelems = (size_t)(p->max_chunk + 7) / 8 * 8 * p->fu_upad;
-    p->d_U = dalloc<double2>(uelems);
+    p->d_U = palloc<double2>(p, uelems);
     CK(cudaMemsetAsync(p->d_U, 0, uelems * 16, s));  // padding rows stay zero
   } else if (p->use_tp) {
-    p->d_U = dalloc<double2>((size_t)p->max_chunk * p->tp_KP);
+    p->d_U = palloc<double2>(p, (size_t)p->max_chunk * p->tp_KP);
     CK(cudaMemsetAsync(p->d_U, 0, (size_t)p->max_chunk * p->tp_KP * 16, s));  // padding rows
   } else if (p->use_ws || p->use_lines) {
     const int gmt = p->use_lines ? 8 : p->ws.MT;
     const size_t groups = (size_t)(p->max_chunk + gmt - 1) / gmt;
-    p->d_U = dalloc<double2>(groups * (size_t)p->ws_stages.group_elems);
+    p->d_U = palloc<double2>(p, groups * (size_t)p->ws_stages.group_elems);
     CK(cudaMemsetAsync(p->d_U, 0, groups * (size_t)p->ws_stages.group_elems * 16, s));
   } else {
-    p->d_U = dalloc<double2>((size_t)p->max_chunk * p->NPQ);
+    p->d_U = palloc<double2>(p, (size_t)p->max_chunk * p->NPQ);
   }
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
@@ -879,12 +947,12 @@ void build_plan(slsht_cuda_plan* p) {
   if (out_bytes + t_bytes + (64u << 20) > free_b)
     throw Status{SLSHT_ERR_VALIDATION,
                  "device output buffer does not fit in HBM (use the streaming ring mode)"};
-  p->d_out = dalloc<double2>((size_t)p->n_slots * p->vstride);
-  if (p->use_tp) p->d_T = dalloc<double2>(t_bytes / 16);
+  p->d_out = palloc<double2>(p, (size_t)p->n_slots * p->vstride);
+  if (p->use_tp) p->d_T = palloc<double2>(p, t_bytes / 16);
   const int parts_per_tile = p->use_fused ? FuCfg<49>::EPW : 1;
-  p->d_partials = dalloc<double>((size_t)p->max_chunk * p->n_col_tiles * parts_per_tile * 8);
+  p->d_partials = palloc<double>(p, (size_t)p->max_chunk * p->n_col_tiles * parts_per_tile * 8);
   p->digest_rows = coeff_count(p->lmax);
-  p->d_digest = dalloc<double>((size_t)p->digest_rows * 8);
+  p->d_digest = palloc<double>(p, (size_t)p->digest_rows * 8);
   for (int i = 0; i < 2; ++i) {
     CK(cudaEventCreateWithFlags(&p->ev_done[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&p->ev_copied[i], cudaEventDisableTiming));
@@ -1307,6 +1375,7 @@ int guarded(slsht_cuda_plan* p, F&& fn) {
     if (p) CK(cudaSetDevice(p->desc.device));
     if (p && p->parts.empty() && p->built) set_func_attributes(p);
     fn();
+    if (p && p->parts.empty() && p->built) check_guards(p);
     return SLSHT_OK;
   } catch (const Status& st) {
     if (p) p->last_error = st.msg;

@@ -1,0 +1,70 @@
+"""Small forwards that launch every kernel of the engine, for bounds checking:
+    SLSHT_CUDA_GUARD=1 python tools/sanitize_cases.py
+With SLSHT_CUDA_GUARD=1 every plan-owned device buffer gets 64-KB guard bands (pattern 0xA5)
+on both sides, verified after every call (a DeviceError names the buffer and the byte); the
+GPU test tests/test_gpu.py::test_guard_bands_every_kernel runs these cases that way and checks
+the results bitwise against unguarded plans. (compute-sanitizer is closed on this GPU pool.)
+Cases: n = 17 (k_couple_ws), 33 (k_couple_lines), 49 (k_tgemm + k_qfft<49>; k_fused with
+SLSHT_CUDA_FUSED=1), 65 (k_qfft<65>), 129 (k_qfft<129>, DMMA radix-43), 225 (k_qfft_rt),
+21 (runtime-plan k_couple<0>), and with them the setup kernels (k_glnodes, k_setup_main,
+k_delta, k_dtab, k_wtab), k_agen, k_modgemm, k_digest, k_inverse."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+import paper_1207_5558_b200 as S  # noqa: E402
+
+CASES = [  # (L_f, L_h, real_mode, lmax, fused)
+    (6, 8, False, 8, False),     # n = 17
+    (4, 16, True, 10, False),    # n = 33, real mode (mirrors)
+    (3, 24, False, 6, False),    # n = 49 two-pass
+    (3, 24, False, 6, True),     # n = 49 fused
+    (2, 32, True, 5, False),     # n = 65, real mode
+    (1, 64, False, 3, False),    # n = 129
+    (1, 112, False, 2, False),   # n = 225, runtime alpha pass
+    (3, 10, False, 6, False),    # n = 21, runtime-plan single-pass kernel
+]
+
+
+def coeffs(rng, L, real):
+    c = rng.standard_normal((L + 1) ** 2) + 1j * rng.standard_normal((L + 1) ** 2)
+    if real:  # f_{l,-m} = (-1)^m conj(f_{l,m})
+        for l in range(L + 1):
+            c[l * l + l] = c[l * l + l].real
+            for m in range(1, l + 1):
+                c[l * l + l - m] = (-1) ** m * np.conj(c[l * l + l + m])
+    return c
+
+
+def run_cases(indices=None):
+    """{case: (digests, captured volumes, inverse)} for the selected cases."""
+    rng = np.random.default_rng(7)
+    out = {}
+    for i, (L_f, L_h, real, lmax, fused) in enumerate(CASES):
+        f, h = coeffs(rng, L_f, real), coeffs(rng, L_h, real)
+        if indices is not None and i not in indices:
+            continue
+        os.environ["SLSHT_CUDA_FUSED"] = "1" if fused else "0"
+        try:
+            with S.Plan(L_f, L_h, real_mode=real, lmax=lmax, ring_bytes=64 << 20) as p:
+                d = p.forward_digests(f, h)
+                d2, v = p.forward_capture(f, h, [(0, 0), (lmax, lmax)])
+                inv = p.inverse(f, h, h[0], L_f)
+                seen = []
+                p.forward_sink(f, h, lambda l, m, vol: seen.append((l, m)))
+        finally:
+            os.environ.pop("SLSHT_CUDA_FUSED", None)
+        assert np.array_equal(d, d2) and len(seen) == len(set(seen))
+        out[i] = (d, v, inv)
+    return out
+
+
+if __name__ == "__main__":
+    res = run_cases()
+    for i, (d, _, _) in res.items():
+        print(f"case {i} {CASES[i]}: digests finite {bool(np.isfinite(d).all())}")
+    S.delta_tables(16)
+    S.delta_tables(180)  # global-memory workspace
+    print("done (guard bands intact)" if os.environ.get("SLSHT_CUDA_GUARD") == "1" else "done")
