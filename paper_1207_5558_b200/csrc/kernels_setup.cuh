@@ -451,11 +451,11 @@ __global__ void k_wtab(int L, const double* __restrict__ h, const double* __rest
   const int NPQ = (L + 1) * (L + 1);
   if (col >= ncol_pad) return;
   for (int c = blockIdx.y; c < NPQ; c += gridDim.y) {  // gridDim.y <= 65535
-    // fu_kp > 0: the fused kernel's column-tile-major layout [col / 16][KR][16] with the K row
+    // fu_kp > 0: the fused kernel's column-tile-major layout [col / 8][KR][8] with the K row
     // wrow[c] of the interleaved row-group layout and XOR-swizzled columns (kernels_fused.cuh)
     auto fused_index = [&](int cl) {
       const int kr = wrow[c];
-      return ((size_t)(cl / 16) * fu_kp + kr) * 16 + ((cl & 8) | ((cl & 7) ^ ((2 * kr) & 7)));
+      return ((size_t)(cl / 8) * fu_kp + kr) * 8 + ((cl & 7) ^ ((2 * kr) & 7));
     };
     if (col >= ncol) {
       W[fu_kp ? fused_index(col)

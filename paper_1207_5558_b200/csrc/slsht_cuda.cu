@@ -1164,6 +1164,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     fp.ncol = p->ncol;
     fp.vol = p->vstride;
     fp.rpitch = p->rpitch;
+    if (const char* e = std::getenv("SLSHT_CUDA_FU_EXP")) fp.exp = std::atoi(e);
     fp.mirror = p->mirror;
     fp.rou = p->d_rou;
     fp.betaw = p->d_betaw;
