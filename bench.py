@@ -433,10 +433,13 @@ def run_ours(args) -> None:
                  "achieved_tflops_canonical": fp64, "peak_tflops": P_FP64_TFLOPS,
                  "frac": fp64 / P_FP64_TFLOPS, "peak_source": FP64_SOURCE}
     step_roof = min(peaks["hbm_gbs"] * 1e9 / 16.0, P_FP64_TFLOPS * 1e12 / cfg.flops_per_sample())
-    traffic = None
+    # measured DRAM traffic of the roofline kernels (committed ncu captures): per launch for a
+    # single-chunk plan, per step (summed over the step's chunks) for the two-pass path
+    traffic, tdoc = None, {}
     tfile = ROOT / "profiles" / f"traffic_config{args.config}.json"
     if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+        tdoc = json.loads(tfile.read_text())
+        traffic = tdoc.get("dram_bytes_per_launch")
     if two_pass:
         # two-pass coupling (n = 49, 65, 129): k_tgemm (FP64 DMMA GEMM, T to HBM) and k_qfft
         # (alpha FFT + epilogue); the roofline kernel is the longer of the two. Algorithmic
@@ -450,13 +453,17 @@ def run_ours(args) -> None:
         tg = {"bound": "tensor", "kernel": "k_tgemm (coupling GEMM on the FP64 tensor cores)",
               "achieved": gemm_flops / (tg_ms / 1e3) / 1e12, "peak": P_FP64_TFLOPS,
               "unit": "TFLOP/s", "frac": gemm_flops / (tg_ms / 1e3) / 1e12 / P_FP64_TFLOPS,
-              "traffic": None, "peak_source": FP64_SOURCE,
+              "traffic": tdoc.get("k_tgemm", {}).get("dram_bytes_per_step"),
+              "traffic_unit": "DRAM bytes per step (ncu, all launches of one step)",
+              "peak_source": FP64_SOURCE,
               "flop_model": "8 FLOP per complex MAC (the DMMA Gauss product issues 6)",
               "algorithmic_flops_per_step": gemm_flops, "kernel_ms_per_step": tg_ms}
         qf = {"bound": "hbm", "kernel": "k_qfft (alpha FFT + store/digest epilogue)",
               "achieved": alg_bytes / (qf_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
               "unit": "GB/s", "frac": alg_bytes / (qf_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
-              "traffic": traffic, "peak_source": peaks["source"],
+              "traffic": tdoc.get("k_qfft", {}).get("dram_bytes_per_step"),
+              "traffic_unit": "DRAM bytes per step (ncu, all launches of one step)",
+              "peak_source": peaks["source"],
               "algorithmic_bytes_per_step": alg_bytes, "kernel_ms_per_step": qf_ms,
               "t_reread_bytes_per_step": t_bytes,
               "moved_gbs_incl_t_reread": (alg_bytes + t_bytes) / (qf_ms / 1e3) / 1e9}
