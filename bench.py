@@ -295,10 +295,23 @@ def run_ours(args) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py: WORLD_SIZE={world} does not match --gpus {args.gpus}")
+    # one rank per GPU over NCCL; BENCH_DIST_BACKEND=gloo (host tensors) lets a one-GPU box run
+    # the multi-rank logic with every rank on that GPU (a plumbing check, not a measurement)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    dev_index = local % max(1, torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # collective tensors
+
+    def reduce_max(x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     f_np, h_np, cfg = C.make_inputs(args.config)
     l0, l1 = C.shard_degrees(cfg, world, rank)
@@ -306,7 +319,7 @@ def run_ours(args) -> None:
     materialize = out_bytes < 40e9
     stream = torch.cuda.Stream(device=dev)
     plan = S.Plan(cfg.L_f, cfg.L_h, real_mode=cfg.real_mode, emit_negative_m=True,
-                  device=local, l_begin=l0, l_end=l1, materialize=materialize,
+                  device=dev_index, l_begin=l0, l_end=l1, materialize=materialize,
                   ring_bytes=args.ring_mb << 20, stream=stream.cuda_stream)
     # inputs resident in HBM (torch is only the allocator here)
     f_dev = torch.from_numpy(f_np.view(np.float64).copy()).to(dev)
@@ -332,7 +345,7 @@ def run_ours(args) -> None:
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev_index) as clocks:
         t_wall = time.perf_counter()
         live = []
         for i in range(args.steps):
@@ -352,10 +365,8 @@ def run_ours(args) -> None:
     total_ms = sum(step_ms)
     launches = launches_per_step * args.steps
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        n = torch.tensor([launches], dtype=torch.int64, device=dev)
+        total_ms = reduce_max(total_ms)
+        n = torch.tensor([launches], dtype=torch.int64, device=cdev)
         dist.all_reduce(n, op=dist.ReduceOp.SUM)
         launches = int(n.item())
         dist.barrier()
@@ -372,11 +383,11 @@ def run_ours(args) -> None:
         g0 = torch.cuda.Event(enable_timing=True)
         g1 = torch.cuda.Event(enable_timing=True)
         g0.record()
-        full_dig = gather_digests(dig_dev, l0, l1, cfg.L_g)
+        full_dig = gather_digests(dig_dev if backend == "nccl" else dig_dev.cpu(), l0, l1, cfg.L_g)
         g1.record()
         torch.cuda.synchronize(dev)
         gather = {"ms": g0.elapsed_time(g1), "rows": int((cfg.L_g + 1) ** 2),
-                  "backend": "nccl all_gather of padded row blocks"}
+                  "backend": f"{backend} all_gather of padded row blocks"}
     rt_err = None
     complete = None
     if rank == 0:
@@ -401,9 +412,7 @@ def run_ours(args) -> None:
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = sum(e2e_times) / len(e2e_times)
     if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = reduce_max(e2e_s)
     r0, r1 = l0 * l0, l1 * l1
     e2e = {"value": total_samples / e2e_s, "unit": "samples/s",
            "h2d_bytes_per_step": int(f_np.nbytes + h_np.nbytes),
@@ -437,7 +446,7 @@ def run_ours(args) -> None:
     # single-chunk plan, per step (summed over the step's chunks) for the two-pass path
     traffic, tdoc = None, {}
     tfile = ROOT / "profiles" / f"traffic_config{args.config}.json"
-    if tfile.exists():
+    if tfile.exists() and world == 1:  # the captures are of the one-GPU plan
         tdoc = json.loads(tfile.read_text())
         traffic = tdoc.get("dram_bytes_per_launch")
     if two_pass:
@@ -503,7 +512,7 @@ def run_ours(args) -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            host_sink = host_sink_sample(S, C, cfg, f_np, h_np, local)
+            host_sink = host_sink_sample(S, C, cfg, f_np, h_np, dev_index)
         except Exception as e:
             host_sink = {"value": None, "error": f"{type(e).__name__}: {e}"}
         try:
