@@ -22,6 +22,7 @@
 #include "kernels_fused.cuh"
 #include "direct.cuh"
 #include "window_solver.cuh"
+#include "blas_fp64.cuh"
 #include "kernels_setup.cuh"
 #include "slsht_cuda.h"
 
@@ -1912,22 +1913,12 @@ double angular_distance(double t1, double p1, double t2, double p2) {
   return std::acos(std::min(1.0, std::max(-1.0, c)));
 }
 
-#define CB(x)                                                                        \
-  do {                                                                               \
-    const cublasStatus_t st_ = (x);                                                  \
-    if (st_ != CUBLAS_STATUS_SUCCESS)                                                \
-      throw Status{SLSHT_ERR_DEVICE, std::string(#x) + ": cuBLAS status " +           \
-                                         std::to_string((int)st_)};                  \
-  } while (0)
-
 }  // namespace
 
 int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int band_limit,
                                     int oversample, double* coeffs, double* lambda_out) {
   std::vector<void*> allocs;
-  cublasHandle_t hb = nullptr;
   auto cleanup = [&]() {
-    if (hb) cublasDestroy(hb);
     for (void* q : allocs) cudaFree(q);
   };
   try {
@@ -1990,20 +1981,17 @@ int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int ba
     double2* d_K = (double2*)dal(sizeof(double2) * (size_t)dim * dim);
     double2* d_v = (double2*)dal(sizeof(double2) * dim);
     double2* d_x = (double2*)dal(sizeof(double2) * dim);
+    double2* d_dn = (double2*)dal(sizeof(double2) * 2);  // v^H x, ||x||
     const int ny = S * (2 * L + 1);
     k_window_y<<<(ny + 127) / 128, 128>>>(L, S, d_t, d_p, d_Y);
     CKL();
     const size_t nb = (size_t)S * dim;
     k_window_scale<<<(unsigned)((nb + 255) / 256), 256>>>(dim, S, d_w, d_Y, d_B);
     CKL();
-    CB(cublasCreate(&hb));
     // row-major Y[s][c] is the column-major dim x S matrix A; K (row-major) = A B^H
     // (column-major), B = A diag(w): K[r][c] = sum_s conj(Y[s][r]) w_s Y[s][c]
-    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
-    CB(cublasZgemm(hb, CUBLAS_OP_N, CUBLAS_OP_C, dim, dim, S, &one,
-                   reinterpret_cast<const cuDoubleComplex*>(d_Y), dim,
-                   reinterpret_cast<const cuDoubleComplex*>(d_B), dim, &zero,
-                   reinterpret_cast<cuDoubleComplex*>(d_K), dim));
+    // (blas_fp64.cuh: DMMA complex GEMM)
+    CK(zgemm(kOpN, kOpC, dim, dim, S, d_Y, dim, d_B, dim, d_K, dim, 0));
     const size_t nk = (size_t)dim * dim;
     k_window_symmetrize<<<(unsigned)((nk + 255) / 256), 256>>>(dim, d_K);
     CKL();
@@ -2016,18 +2004,17 @@ int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int ba
     bool converged = false;
     for (int it = 0; it < 100000; ++it) {
       // w = K v: K row-major is the column-major K^T
-      CB(cublasZgemv(hb, CUBLAS_OP_T, dim, dim, &one, reinterpret_cast<cuDoubleComplex*>(d_K),
-                     dim, reinterpret_cast<cuDoubleComplex*>(d_v), 1, &zero,
-                     reinterpret_cast<cuDoubleComplex*>(d_x), 1));
-      cuDoubleComplex rq;
-      double nw = 0.0;
-      CB(cublasZdotc(hb, dim, reinterpret_cast<cuDoubleComplex*>(d_v), 1,
-                     reinterpret_cast<cuDoubleComplex*>(d_x), 1, &rq));
-      CB(cublasDznrm2(hb, dim, reinterpret_cast<cuDoubleComplex*>(d_x), 1, &nw));
-      lambda = cuCreal(rq);
+      k_zgemv_t<<<(dim * 32 + 255) / 256, 256>>>(dim, d_K, dim, d_v, d_x);
+      CKL();
+      k_zdot_nrm<<<1, 1024>>>(dim, d_v, d_x, d_dn);
+      CKL();
+      double2 dn[2];
+      CK(cudaMemcpy(dn, d_dn, sizeof dn, cudaMemcpyDeviceToHost));
+      const double nw = dn[1].x;
+      lambda = dn[0].x;
       if (nw == 0.0) throw Status{SLSHT_ERR_NUMERIC, "power iteration collapsed to zero"};
-      const double inv = 1.0 / nw;
-      CB(cublasZdscal(hb, dim, &inv, reinterpret_cast<cuDoubleComplex*>(d_x), 1));
+      k_zscale_inv<<<(dim + 255) / 256, 256>>>(dim, d_dn, d_x);
+      CKL();
       std::swap(d_v, d_x);
       if (it > 0 && std::fabs(lambda - lambda_prev) <= 1e-12 * std::fabs(lambda)) {
         converged = true;
@@ -2092,10 +2079,8 @@ int slsht_cuda_eigenfunction_window(int device, double theta_c, double a, int ba
 int slsht_cuda_forward_direct(int device, int L_f, const double* f, int L_h, const double* h,
                               int lmax, const long long* cells, long long ncells, double* out) {
   std::vector<void*> allocs;
-  cublasHandle_t hb = nullptr;
   cudaStream_t s = nullptr;
   auto cleanup = [&]() {
-    if (hb) cublasDestroy(hb);
     if (s) cudaStreamDestroy(s);
     for (void* q : allocs) cudaFree(q);
   };
@@ -2115,8 +2100,6 @@ int slsht_cuda_forward_direct(int device, int L_f, const double* f, int L_h, con
       throw Status{SLSHT_ERR_DEVICE, "no CUDA device available (the engine has no CPU fallback)"};
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    CB(cublasCreate(&hb));
-    CB(cublasSetStream(hb, s));
     auto dal = [&](size_t bytes) {
       void* q = nullptr;
       CK(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
@@ -2199,16 +2182,14 @@ int slsht_cuda_forward_direct(int device, int L_f, const double* f, int L_h, con
       qm_off[m + lmax + 1] = qm_off[m + lmax] + (size_t)(lmax - std::abs(m) + 1) * nt;
     double* d_Q = (double*)dal(8 * qm_off.back());
     double* d_la = (double*)dal(8 * (size_t)(lmax + 1) * NN);
-    const double one = 1.0, zero = 0.0;
     for (int m = -lmax; m <= lmax; ++m) {
       const int nl = lmax - std::abs(m) + 1;
       k_dir_lrows<<<blocks(NN, 128), 128, 3 * (lmax + 2) * 8, s>>>(m, lmax, NN, d_nodes, d_wq, d_la,
                                                                   NN);
       CKL();
       // row-major Q (nl x nt) = Lambda (nl x NN) B (NN x nt): column-major Q^T = B^T Lambda^T
-      CB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, nt, nl, NN, &one,
-                     d_B + (size_t)(m & 1) * NN * nt, nt, d_la, NN, &zero, d_Q + qm_off[m + lmax],
-                     nt));
+      CK(dgemm(kOpN, kOpN, nt, nl, NN, d_B + (size_t)(m & 1) * NN * nt, nt, d_la, NN,
+               d_Q + qm_off[m + lmax], nt, s));
     }
     // ---- cells in batches of R
     const size_t per_r = 16 * ((size_t)NPQ + (size_t)nt * nh + 2 * (size_t)nt * n +
@@ -2224,7 +2205,6 @@ int slsht_cuda_forward_direct(int device, int L_f, const double* f, int L_h, con
     double2* d_res = (double2*)dal(16 * (size_t)coeff_count(lmax) * R);
     long long* d_cells = (long long*)dal(8 * (size_t)R);
     std::vector<long long> hcells(R);
-    const cuDoubleComplex zone = make_cuDoubleComplex(1.0, 0.0), zzero = make_cuDoubleComplex(0.0, 0.0);
     for (long long c0 = 0; c0 < ncells; c0 += R) {
       const int r = (int)std::min<long long>(R, ncells - c0);
       for (int i = 0; i < r; ++i) {
@@ -2238,34 +2218,28 @@ int slsht_cuda_forward_direct(int device, int L_f, const double* f, int L_h, con
       // S[t][q][r] = sum_p lambda_p^q(theta_t) HR[(p,q)][r]  (real x complex: 2r real columns)
       for (int jq = 0; jq < nh; ++jq) {
         const int kq = qoff[jq + 1] - qoff[jq];
-        CB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, 2 * r, nt, kq, &one,
-                       reinterpret_cast<const double*>(d_HR + (size_t)qoff[jq] * r), 2 * r,
-                       d_ls + (size_t)qoff[jq] * nt, nt, &zero,
-                       reinterpret_cast<double*>(d_S + (size_t)jq * r), 2 * nh * r));
+        CK(dgemm(kOpN, kOpT, 2 * r, nt, kq,
+                 reinterpret_cast<const double*>(d_HR + (size_t)qoff[jq] * r), 2 * r,
+                 d_ls + (size_t)qoff[jq] * nt, nt, reinterpret_cast<double*>(d_S + (size_t)jq * r),
+                 2 * nh * r, s));
       }
       // H[t][k][r] = sum_q Esyn[k][q] S[t][q][r]
-      CB(cublasZgemmStridedBatched(hb, CUBLAS_OP_N, CUBLAS_OP_N, r, n, nh, &zone,
-                                   reinterpret_cast<const cuDoubleComplex*>(d_S), r,
-                                   (long long)nh * r,
-                                   reinterpret_cast<const cuDoubleComplex*>(d_esyn), nh, 0, &zzero,
-                                   reinterpret_cast<cuDoubleComplex*>(d_H), r, (long long)n * r, nt));
+      CK(zgemm(kOpN, kOpN, r, n, nh, d_S, r, d_esyn, nh, d_H, r, s, nt, (long long)nh * r, 0,
+               (long long)n * r));
       const long long tot = (long long)nt * n * r;
       k_dir_product<<<blocks(tot, 256), 256, 0, s>>>(tot, r, d_F, d_H);
       CKL();
       // FM[t][m][r] = sum_k Eana[m][k] P[t][k][r]
-      CB(cublasZgemmStridedBatched(hb, CUBLAS_OP_N, CUBLAS_OP_N, r, n, n, &zone,
-                                   reinterpret_cast<const cuDoubleComplex*>(d_H), r,
-                                   (long long)n * r,
-                                   reinterpret_cast<const cuDoubleComplex*>(d_eana), n, 0, &zzero,
-                                   reinterpret_cast<cuDoubleComplex*>(d_FM), r, (long long)n * r, nt));
+      CK(zgemm(kOpN, kOpN, r, n, n, d_H, r, d_eana, n, d_FM, r, s, nt, (long long)n * r, 0,
+               (long long)n * r));
       // OUT[m][l - |m|][r] = sum_t Q_m[l][t] FM[t][m][r]
       for (int m = -lmax; m <= lmax; ++m) {
         const int nl = lmax - std::abs(m) + 1;
-        CB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, 2 * r, nl, nt, &one,
-                       reinterpret_cast<const double*>(d_FM + (size_t)(m + L) * r), 2 * n * r,
-                       d_Q + qm_off[m + lmax], nt, &zero,
-                       reinterpret_cast<double*>(d_OUT + (size_t)(m + lmax) * (lmax + 1) * r),
-                       2 * r));
+        CK(dgemm(kOpN, kOpN, 2 * r, nl, nt,
+                 reinterpret_cast<const double*>(d_FM + (size_t)(m + L) * r), 2 * n * r,
+                 d_Q + qm_off[m + lmax], nt,
+                 reinterpret_cast<double*>(d_OUT + (size_t)(m + lmax) * (lmax + 1) * r), 2 * r,
+                 s));
       }
       const long long nres = (long long)coeff_count(lmax) * r;
       k_dir_scatter<<<blocks(nres, 256), 256, 0, s>>>(lmax, r, nres, d_OUT, d_res);

@@ -14,7 +14,6 @@
 //      (window.cpp:159-196).
 #pragma once
 
-#include <cublas_v2.h>
 
 #include <complex>
 
