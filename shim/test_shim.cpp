@@ -239,6 +239,13 @@ int main() {
     unsetenv("SLSHT_CUDA_PLAN_CACHE");
     const double d = std::max({max_diff(a1, a2), max_diff(b1, b2), max_diff(a1, a3)});
     report(d == 0.0, "plan cache: repeated calls bitwise equal to fresh plans", d, 0.0);
+    // device selection: two degree shards (here both on device 0, the test box's one GPU)
+    // give bitwise the one-device result, through the multi-GPU plan of the C ABI
+    setenv("SLSHT_CUDA_DEVICES", "0,0", 1);
+    const SlshtDistribution a4 = forward_fast(f, h);
+    unsetenv("SLSHT_CUDA_DEVICES");
+    const double d4 = max_diff(a1, a4);
+    report(d4 == 0.0, "two-shard plan (SLSHT_CUDA_DEVICES) bitwise equal to one device", d4, 0.0);
   }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ALL PASSED", failures);
   return failures ? 1 : 0;
