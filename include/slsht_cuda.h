@@ -162,6 +162,22 @@ int slsht_cuda_kernel_time(const slsht_cuda_plan* plan, double* ms);
  * DeltaTables (wigner.cpp:28-80), ModulatedSht::compute (transform.cpp:189-220) and the
  * window-side table of the coupling stage; used by the parity tests. */
 int slsht_cuda_delta_tables(int device, int L, double* out);
+
+/* Grid functions of the path on the device (component-level, as the engine computes them):
+ *  - theta_weights(N): the N+1 colatitude weights of S_N (proj/src/grids.cpp:76-92),
+ *    SLSHT_ERR_NUMERIC on an imaginary residue >= 1e-12 (grids.cpp:86-89);
+ *  - beta_weights(L): the L+1 weights q(beta_b) of the inverse (grids.cpp:54-74);
+ *  - legendre_rows(m, lmax, thetas, n): rows[(l-|m|) n + j] = lambda_l^m(theta_j) for
+ *    |m| <= l <= lmax (proj/src/harmonics.cpp:60-89), (lmax-|m|+1) x n doubles;
+ *  - gauss_legendre_half(points): the x = cos(theta) >= 0 half of the points-point
+ *    Gauss-Legendre rule the engine's modulated SHT integrates with ((points+1)/2 nodes,
+ *    decreasing x; the x = 0 node of an odd rule carries half its weight). */
+int slsht_cuda_theta_weights(int device, int N, double* out);
+int slsht_cuda_beta_weights(int device, int L, double* out);
+int slsht_cuda_legendre_rows(int device, int m, int lmax, const double* thetas, int n,
+                             double* rows);
+int slsht_cuda_gauss_legendre_half(int device, int points, double* ncos, double* nsin,
+                                   double* weights);
 /* mod for (l[i], m[i]), i < count: out is count x coeff_count(L_h) complex, coeff_index(p, q). */
 int slsht_cuda_modulated(slsht_cuda_plan* plan, const double* f, int count, const int* l,
                          const int* m, double* out);

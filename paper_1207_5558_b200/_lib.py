@@ -44,6 +44,10 @@ EXPORTS = [
     "slsht_cuda_copy_sink",
     "slsht_cuda_shard_bounds",
     "slsht_cuda_device_count",
+    "slsht_cuda_theta_weights",
+    "slsht_cuda_beta_weights",
+    "slsht_cuda_legendre_rows",
+    "slsht_cuda_gauss_legendre_half",
 ]
 
 
@@ -123,6 +127,14 @@ def load() -> C.CDLL:
     lib.slsht_cuda_kernel_time.restype = C.c_int
     lib.slsht_cuda_delta_tables.argtypes = [C.c_int, C.c_int, _dp]
     lib.slsht_cuda_delta_tables.restype = C.c_int
+    lib.slsht_cuda_theta_weights.argtypes = [C.c_int, C.c_int, _dp]
+    lib.slsht_cuda_theta_weights.restype = C.c_int
+    lib.slsht_cuda_beta_weights.argtypes = [C.c_int, C.c_int, _dp]
+    lib.slsht_cuda_beta_weights.restype = C.c_int
+    lib.slsht_cuda_legendre_rows.argtypes = [C.c_int, C.c_int, C.c_int, _dp, C.c_int, _dp]
+    lib.slsht_cuda_legendre_rows.restype = C.c_int
+    lib.slsht_cuda_gauss_legendre_half.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp]
+    lib.slsht_cuda_gauss_legendre_half.restype = C.c_int
     lib.slsht_cuda_eigenfunction_window.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int,
                                                     C.c_int, C.c_void_p, _dp]
     lib.slsht_cuda_eigenfunction_window.restype = C.c_int

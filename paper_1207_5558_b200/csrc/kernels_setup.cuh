@@ -261,6 +261,57 @@ __global__ void __launch_bounds__(128) k_setup_main(const SetupMainParams P) {
   }
 }
 
+// Component-level entry points of the grid functions (slsht_cuda_theta_weights,
+// slsht_cuda_beta_weights, slsht_cuda_legendre_rows): the same device code as the setup
+// launch, one warp per weight / one thread per angle.
+__global__ void k_theta_weights(int N, double* __restrict__ out, int* __restrict__ err) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (t > N) return;
+  const double theta = kPi * (2 * t + 1) / (2 * N + 1);  // grids.cpp:79-80
+  double sr, si;
+  quad_weight_sum(N, theta, lane, sr, si);
+  if (lane == 0) {
+    if (fabs(si) >= 1e-12) atomicExch(err, 1);
+    out[t] = (t < N) ? 2.0 * sr / (2 * N + 1) : sr / (2 * N + 1);
+  }
+}
+
+__global__ void k_beta_weights(int L, double* __restrict__ out, int* __restrict__ err) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (t > L) return;
+  const int n = 2 * L + 1;
+  if (t == 0) {
+    if (lane == 0) out[0] = 4.0 * kPi * kPi / (L / 2 + 0.5);
+    return;
+  }
+  double sr, si;
+  quad_weight_sum(L, 2.0 * kPi * t / n, lane, sr, si);
+  if (lane == 0) {
+    if (fabs(si) >= 1e-12) atomicExch(err, 2);
+    out[t] = 8.0 * kPi * kPi * sr;
+  }
+}
+
+// rows[(l - |m|) n + j] = lambda_l^m(theta_j), |m| <= l <= lmax (harmonics.cpp:60-89)
+__global__ void k_legendre_rows(int m, int lmax, const double* __restrict__ thetas, int n,
+                                double* __restrict__ rows) {
+  extern __shared__ double coef[];
+  double *sf = coef, *ca = coef + (lmax + 1), *cb = coef + 2 * (lmax + 1);
+  const int am = m < 0 ? -m : m;
+  legendre_coeffs(am, lmax, sf, ca, cb);
+  __syncthreads();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double c, s;
+  sincos(thetas[j], &s, &c);
+  LegendreIt r;
+  r.seed(m, c, s, sf);
+  for (int l = am; l <= lmax; ++l) {
+    if (l > am) r.next(ca, cb);
+    rows[(size_t)(l - am) * n + j] = r.cur;
+  }
+}
+
 __device__ __forceinline__ size_t delta_offset(int p) {
   return (size_t)p * (2 * p - 1) * (2 * p + 1) / 3;
 }

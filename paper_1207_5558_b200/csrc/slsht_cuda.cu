@@ -2265,6 +2265,132 @@ int slsht_cuda_forward_direct(int device, int L_f, const double* f, int L_h, con
   }
 }
 
+}  // extern "C"
+
+namespace {
+// run fn on `device` with the ABI's error mapping (component-level entry points)
+template <class F>
+int on_device(int device, F&& fn) {
+  std::vector<void*> allocs;
+  auto dal = [&](size_t bytes) {
+    void* q = nullptr;
+    CK(cudaMalloc(&q, bytes ? bytes : 1));
+    allocs.push_back(q);
+    return q;
+  };
+  auto cleanup = [&]() {
+    for (void* q : allocs) cudaFree(q);
+  };
+  try {
+    int dev_count = 0;
+    if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+      throw Status{SLSHT_ERR_DEVICE, "no CUDA device available (the engine has no CPU fallback)"};
+    if (device < 0 || device >= dev_count) throw Status{SLSHT_ERR_DEVICE, "invalid device ordinal"};
+    CK(cudaSetDevice(device));
+    fn(dal);
+    cleanup();
+    return SLSHT_OK;
+  } catch (const Status& st) {
+    cleanup();
+    g_create_error = st.msg;
+    return st.code;
+  } catch (const CudaError& e) {
+    cleanup();
+    g_create_error = e.msg;
+    return SLSHT_ERR_DEVICE;
+  } catch (const std::exception& e) {
+    cleanup();
+    g_create_error = e.what();
+    return SLSHT_ERR_DEVICE;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int slsht_cuda_theta_weights(int device, int N, double* out) {
+  if (N < 0 || !out) {
+    g_create_error = N < 0 ? "quadrature order must be non-negative" : "null output";
+    return SLSHT_ERR_VALIDATION;
+  }
+  return on_device(device, [&](auto dal) {
+    double* d = (double*)dal(sizeof(double) * (N + 1));
+    int* err = (int*)dal(sizeof(int));
+    CK(cudaMemset(err, 0, sizeof(int)));
+    k_theta_weights<<<(N + 1 + 3) / 4, 128>>>(N, d, err);
+    CKL();
+    int herr = 0;
+    CK(cudaMemcpy(&herr, err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (herr)  // grids.cpp:86-89
+      throw Status{SLSHT_ERR_NUMERIC, "theta_weights: imaginary residue above tolerance"};
+    CK(cudaMemcpy(out, d, sizeof(double) * (N + 1), cudaMemcpyDeviceToHost));
+  });
+}
+
+int slsht_cuda_beta_weights(int device, int L, double* out) {
+  if (L < 0 || !out) {
+    g_create_error = L < 0 ? "band limit must be non-negative" : "null output";
+    return SLSHT_ERR_VALIDATION;
+  }
+  return on_device(device, [&](auto dal) {
+    double* d = (double*)dal(sizeof(double) * (L + 1));
+    int* err = (int*)dal(sizeof(int));
+    CK(cudaMemset(err, 0, sizeof(int)));
+    k_beta_weights<<<(L + 1 + 3) / 4, 128>>>(L, d, err);
+    CKL();
+    int herr = 0;
+    CK(cudaMemcpy(&herr, err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (herr)  // grids.cpp:66-69
+      throw Status{SLSHT_ERR_NUMERIC, "beta_weights: imaginary residue above tolerance"};
+    CK(cudaMemcpy(out, d, sizeof(double) * (L + 1), cudaMemcpyDeviceToHost));
+  });
+}
+
+int slsht_cuda_legendre_rows(int device, int m, int lmax, const double* thetas, int n,
+                             double* rows) {
+  if (lmax < 0 || std::abs(m) > lmax || n < 0 || (n > 0 && (!thetas || !rows))) {
+    g_create_error = "legendre_rows requires |m| <= lmax and n >= 0";
+    return SLSHT_ERR_VALIDATION;
+  }
+  if (n == 0) return SLSHT_OK;
+  return on_device(device, [&](auto dal) {
+    const int nl = lmax - std::abs(m) + 1;
+    double* dt = (double*)dal(sizeof(double) * n);
+    double* dr = (double*)dal(sizeof(double) * (size_t)nl * n);
+    CK(cudaMemcpy(dt, thetas, sizeof(double) * n, cudaMemcpyHostToDevice));
+    const size_t sm = sizeof(double) * 3 * (lmax + 1);
+    if (sm > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_legendre_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sm));
+    k_legendre_rows<<<(n + 127) / 128, 128, sm>>>(m, lmax, dt, n, dr);
+    CKL();
+    CK(cudaMemcpy(rows, dr, sizeof(double) * (size_t)nl * n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int slsht_cuda_gauss_legendre_half(int device, int points, double* ncos, double* nsin,
+                                   double* weights) {
+  if (points < 1 || !ncos || !nsin || !weights) {
+    g_create_error = points < 1 ? "the rule needs at least one point" : "null output";
+    return SLSHT_ERR_VALIDATION;
+  }
+  if (4 * sizeof(double) * (points + 1) > 227 * 1024) {
+    g_create_error = "rule too large for the node recursion table";
+    return SLSHT_ERR_VALIDATION;
+  }
+  return on_device(device, [&](auto dal) {
+    const int K = (points + 1) / 2;
+    double* d = (double*)dal(sizeof(double) * 3 * K);
+    const size_t sm = 4 * sizeof(double) * (points + 1);
+    CK(cudaFuncSetAttribute(k_glnodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_glnodes<<<(K + 63) / 64, 64, sm>>>(points, K, d, d + K, d + 2 * K);
+    CKL();
+    CK(cudaMemcpy(ncos, d, sizeof(double) * K, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(nsin, d + K, sizeof(double) * K, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(weights, d + 2 * K, sizeof(double) * K, cudaMemcpyDeviceToHost));
+  });
+}
+
 int slsht_cuda_delta_tables(int device, int L, double* out) {
   double* d = nullptr;
   try {

@@ -313,6 +313,44 @@ def shard_bounds(l_begin: int, l_end: int, real_mode: bool, parts: int) -> list[
     return list(out)
 
 
+def theta_weights(N: int, device: int = 0) -> np.ndarray:
+    """theta_weights(N) (grids.cpp:76-92) on the device: the N+1 weights of S_N."""
+    lib = L.load()
+    out = np.zeros(max(N + 1, 0))
+    _raise(lib.slsht_cuda_theta_weights(device, N, out.ctypes.data_as(L._dp)), None)
+    return out
+
+
+def beta_weights(band_limit: int, device: int = 0) -> np.ndarray:
+    """beta_weights(L) (grids.cpp:54-74) on the device: q(beta_b), b <= L."""
+    lib = L.load()
+    out = np.zeros(max(band_limit + 1, 0))
+    _raise(lib.slsht_cuda_beta_weights(device, band_limit, out.ctypes.data_as(L._dp)), None)
+    return out
+
+
+def legendre_rows(m: int, lmax: int, thetas, device: int = 0) -> np.ndarray:
+    """legendre_rows (harmonics.cpp:60-89) on the device: [lmax-|m|+1, len(thetas)]."""
+    lib = L.load()
+    th = np.ascontiguousarray(thetas, np.float64)
+    out = np.zeros((max(lmax - abs(m) + 1, 0), th.size))
+    _raise(lib.slsht_cuda_legendre_rows(device, m, lmax, th.ctypes.data_as(L._dp), th.size,
+                                        out.ctypes.data_as(L._dp)), None)
+    return out
+
+
+def gauss_legendre_half(points: int, device: int = 0):
+    """The x >= 0 half of the points-point Gauss-Legendre rule of the modulated SHT
+    (DESIGN.md §2): (cos, sin, weights), (points+1)//2 nodes, decreasing x."""
+    lib = L.load()
+    K = (points + 1) // 2
+    c, s, w = np.zeros(K), np.zeros(K), np.zeros(K)
+    _raise(lib.slsht_cuda_gauss_legendre_half(device, points, c.ctypes.data_as(L._dp),
+                                              s.ctypes.data_as(L._dp), w.ctypes.data_as(L._dp)),
+           None)
+    return c, s, w
+
+
 def delta_tables(band_limit: int, device: int = 0) -> np.ndarray:
     """Delta^p = d^p(pi/2), p <= band_limit, flat in the reference's layout (wigner.hpp:20-30)."""
     lib = L.load()
