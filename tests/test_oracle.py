@@ -212,3 +212,43 @@ def test_oracle_matches_live_reference(oracle_lib, reference_lib):
         b = reference_lib.forward_fast(f, L_f, real, h, L_h, real, threads=3)
         assert sorted(a) == sorted(b)
         assert max(np.max(np.abs(a[k] - b[k])) for k in b) == 0.0  # bit-identical restatement
+
+
+def test_gauss_legendre_half_rule_equals_reference_quadrature(oracle_lib):
+    """The engine integrates the modulated SHT over theta with the x >= 0 half of the
+    (L_g + 1)-point Gauss-Legendre rule (DESIGN.md §2) instead of the reference's S_{2L_g}
+    rule (transform.cpp:151-156, 206-219): both are exact for the integrand, so in long double
+    they agree to roundoff, and in double the engine's rule is at least as accurate
+    (tools/quadrature_check.py, CPU)."""
+    import sys
+    from pathlib import Path
+
+    import numpy as np
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+    import quadrature_check as Q
+
+    LD = np.longdouble
+    rng = np.random.default_rng(5)
+    L_f, L_h = 40, 6
+    L_g = L_f + L_h
+    f = np.concatenate([(rng.standard_normal(2 * p + 1) + 1j * rng.standard_normal(2 * p + 1))
+                        / (p + 1) for p in range(L_f + 1)])
+    cL, sL, wL = Q.gl_full(L_g + 1, LD)
+    keep = cL > 1e-12
+    if (L_g + 1) % 2:
+        keep[int(np.argmin(np.abs(cL)))] = True
+    cD, sD, wD = (a[keep].astype(np.float64) for a in (cL, sL, wL))
+    if (L_g + 1) % 2:
+        j = int(np.argmin(np.abs(cD)))
+        cD[j], sD[j], wD[j] = 0.0, 1.0, wD[j] * 0.5
+    for l, m in [(L_g, -1), (L_g - 2, 7), (10, 3), (0, 0)]:
+        truth = Q.modulated(f, L_f, L_h, l, m, cL, sL, wL, LD, False)
+        truth_mw = Q.modulated(f, L_f, L_h, l, m, *Q.mw(2 * L_g, LD), LD, False)
+        eng = Q.modulated(f, L_f, L_h, l, m, cD, sD, wD, np.float64, True)
+        ref = oracle_lib.modulated_sht(f, L_f, l, m, L_h)
+        sc = float(np.max(np.abs(truth)))
+        assert float(np.max(np.abs(truth - truth_mw))) / sc < 1e-15  # both rules exact
+        e_eng = float(np.max(np.abs(eng - truth))) / sc
+        e_ref = float(np.max(np.abs(ref - truth))) / sc
+        assert e_eng < 1e-13 and e_eng <= max(2 * e_ref, 1e-15), (l, m, e_eng, e_ref)
