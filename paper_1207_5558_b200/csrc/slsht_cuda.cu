@@ -19,6 +19,7 @@
 #include "kernels_couple_ws.cuh"
 #include "kernels_couple_lines.cuh"
 #include "kernels_twopass.cuh"
+#include "kernels_tpipe.cuh"
 #include "kernels_fused.cuh"
 #include "direct.cuh"
 #include "window_solver.cuh"
@@ -145,6 +146,14 @@ struct slsht_cuda_plan {
   bool tp_col_fast = false; //  k_tgemm raster: column tiles fastest (W L2-resident)
   bool tp_t_stream = false; //  k_tgemm: T stores with the evict-first hint
   size_t tp_t_elems = 0;   //   one T buffer (two in the overlapped schedule)
+  bool tp_pipe = false;    //   k_tpipe: GEMM and alpha-pass items in one persistent kernel over an
+                           //   L2-resident ring of T slots (kernels_tpipe.cuh; n = 49, 65)
+  int tp_ct = 0, tp_ncg = 0, tp_nqg = 0, tp_nslot = 3, tp_fb = 8, tp_lag = 1;
+  size_t tp_slot_elems = 0, tp_pipe_smem = 0;
+  int tp_sync_ints = 0;
+  int* d_tp_sync = nullptr;
+  int* d_qg = nullptr;     //   k-step bounds of the q groups
+  void (*tp_pipe_fn)(TpParams) = nullptr;
   cudaStream_t fft_stream = nullptr;
   cudaEvent_t ev_tg[2] = {}, ev_fft[2] = {};
   bool fft_rec[2] = {false, false};  // ev_fft[b] recorded during the current call
@@ -284,6 +293,8 @@ void free_plan(slsht_cuda_plan* p) {
   pfree(p, p->d_f);
   pfree(p, p->d_T);
   pfree(p, p->d_qend);
+  pfree(p, p->d_tp_sync);
+  pfree(p, p->d_qg);
   pfree(p, p->d_wrow);
   pfree(p, p->d_r43);
   pfree(p, p->d_h);
@@ -466,6 +477,7 @@ void set_func_attributes(const slsht_cuda_plan* p) {
   } else if (p->use_tp) {
     opt(tgemm_variant(p->tp_gv).fn, p->tp_gemm_smem);
     opt(p->tp_fft, p->tp_fft_smem);
+    if (p->tp_pipe) opt(p->tp_pipe_fn, p->tp_pipe_smem);
   } else if (p->use_ws) {
     opt(p->ws.fn, p->couple_smem);
   } else {
@@ -943,6 +955,54 @@ void build_plan(slsht_cuda_plan* p) {
       p->tp_bn = 32;
     }
     p->tp_t_elems = (size_t)p->max_chunk * p->n * p->tp_ncolp;
+    // k_tpipe (kernels_tpipe.cuh): one persistent kernel over an L2-resident ring of T slots.
+    // SLSHT_CUDA_TP_PIPE=0/1 forces either path; _CT / _NQG / _NSLOT / _FB override the shape.
+    {
+      const char* e = std::getenv("SLSHT_CUDA_TP_PIPE");
+      p->tp_pipe = (p->n == 49 || p->n == 65) && p->tp_bn == TP_BN && !p->tp_overlap && e && e[0] == '1';
+    }
+    if (p->tp_pipe) {
+      auto env_int = [](const char* name, int dflt) {
+        const char* e = std::getenv(name);
+        return e ? std::atoi(e) : dflt;
+      };
+      p->tp_pipe_fn = p->n == 49 ? k_tpipe<49> : k_tpipe<65>;
+      const int nct = p->tp_ncolp / TP_BN;
+      const size_t tile_bytes = (size_t)TG_BM * p->n * TP_BN * 16;
+      int ct = env_int("SLSHT_CUDA_TP_CT", (int)std::max<size_t>(1, (20u << 20) / tile_bytes));
+      ct = std::max(1, std::min(ct, nct));
+      p->tp_ncg = (nct + ct - 1) / ct;
+      p->tp_ct = (nct + p->tp_ncg - 1) / p->tp_ncg;
+      p->tp_lag = std::max(1, env_int("SLSHT_CUDA_TP_LAG", 1));
+      p->tp_nslot = std::max(p->tp_lag + 1, env_int("SLSHT_CUDA_TP_NSLOT", p->tp_lag + 2));
+      p->tp_fb = env_int("SLSHT_CUDA_TP_FB", 8);
+      if (p->tp_fb < 1 || TG_BM % p->tp_fb) p->tp_fb = 8;
+      // q groups: consecutive q (whole k-step ranges) with about equal k-step counts
+      std::vector<int> qe;  // k-step after each q's last
+      for (size_t k = 0; k < qend.size(); ++k)
+        if (qend[k] >= 0) qe.push_back((int)k + 1);
+      const int nks = qe.empty() ? 0 : qe.back();
+      int nqg = env_int("SLSHT_CUDA_TP_NQG", std::max(1, (nks + 11) / 22));
+      nqg = std::max(1, std::min<int>(nqg, (int)qe.size()));
+      std::vector<int> qg(1, 0);
+      for (size_t i = 0; i < qe.size(); ++i) {
+        const int g = (int)qg.size();  // closing group g (1-based) at its target
+        if (g < nqg && (long long)qe[i] * nqg >= (long long)nks * g &&
+            (int)(qe.size() - 1 - i) >= nqg - g)
+          qg.push_back(qe[i]);
+      }
+      qg.push_back(nks);
+      // (degenerate targets can leave fewer groups than asked for)
+      qg.erase(std::unique(qg.begin(), qg.end()), qg.end());
+      p->tp_nqg = (int)qg.size() - 1;
+      p->d_qg = dupload(qg, s);
+      p->tp_slot_elems = (size_t)TG_BM * p->n * p->tp_ct * TP_BN;
+      p->tp_t_elems = p->tp_slot_elems * p->tp_nslot;
+      const int nsub_max = ((p->max_chunk + TG_BM - 1) / TG_BM) * p->tp_ncg;
+      p->tp_sync_ints = 1 + nsub_max * (1 + p->tp_ct);
+      p->d_tp_sync = palloc<int>(p, p->tp_sync_ints);
+      p->tp_pipe_smem = tpipe_smem_bytes(p->n, p->tp_KP);
+    }
   }
   const size_t t_bytes = p->use_tp ? p->tp_t_elems * 16 * (p->tp_overlap ? 2 : 1) : 0;
   if (out_bytes + t_bytes + (64u << 20) > free_b)
@@ -1237,6 +1297,47 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
       }
     }
 #endif
+  } else if (p->use_tp && p->tp_pipe) {
+    TpParams tp{};
+    tp.U = p->d_U;
+    tp.W = p->d_W;
+    tp.T = p->d_T;
+    tp.qend = p->d_qend;
+    tp.count = ch.count;
+    tp.KP = p->tp_KP;
+    tp.wpitch = p->tp_ncolp;
+    tp.n = p->n;
+    tp.sync = p->d_tp_sync;
+    tp.qg = p->d_qg;
+    tp.nblk = (ch.count + TG_BM - 1) / TG_BM;
+    tp.ncg = p->tp_ncg;
+    tp.CT = p->tp_ct;
+    tp.nct = p->tp_ncolp / TP_BN;
+    tp.nqg = p->tp_nqg;
+    tp.nslot = p->tp_nslot;
+    tp.fb = p->tp_fb;
+    tp.lag = p->tp_lag;
+    if (const char* e = std::getenv("SLSHT_CUDA_TP_EXP")) tp.exp = std::atoi(e);
+    tp.slot_elems = (long long)p->tp_slot_elems;
+    tp.tpitch = p->tp_ct * TP_BN;
+    tp.out = p->d_out;
+    tp.partials = p->d_partials;
+    tp.comps = comps;
+    tp.ncol = p->ncol;
+    tp.n_tiles = p->tp_ntiles;
+    tp.vol = p->vstride;
+    tp.rpitch = p->rpitch;
+    tp.mirror = p->mirror;
+    tp.rou = p->d_rou;
+    tp.perm = p->d_perm;
+    tp.betaw = p->d_betaw;
+    CK(cudaMemsetAsync(p->d_tp_sync, 0, sizeof(int) * (1 + (size_t)tp.nblk * tp.ncg * (1 + tp.CT)), s));
+    int grid = 3 * p->num_sms;
+    if (const char* g = std::getenv("SLSHT_CUDA_TP_GRID")) grid = std::max(1, std::atoi(g));
+    p->tp_pipe_fn<<<grid, TP_THREADS, p->tp_pipe_smem, s>>>(tp);
+    CKL();
+    record(p, 5);
+    p->launches += 1;
   } else if (p->use_tp) {
     // overlapped schedule: T buffer b = chunk parity; k_tgemm waits until the k_qfft that read
     // T[b] two chunks ago is done, and k_qfft + digest run on fft_stream
