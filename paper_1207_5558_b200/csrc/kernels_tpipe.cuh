@@ -87,7 +87,11 @@ __device__ __forceinline__ void cta_signal_counter(int* p, int tid) {
   }
 }
 
-template <int N>
+// FV = 0: k_qfft's tile body (cp.async tile, FftDif in shared memory, epilogue pass): digests
+// bitwise equal to k_qfft's. FV = 1: the lean alpha pass for N = R1 R2: the first DIF stage reads
+// its rows straight from L2 into registers and writes the tile once; the last stage's outputs go
+// from registers to the volume rows (and the digest), per-warp digest partials (4 per tile).
+template <int N, int FV>
 __global__ void __launch_bounds__(TP_THREADS, 3) k_tpipe(const TpParams P) {
   constexpr int NTHR = TP_THREADS, BN = TP_BN, WNF = 2, NST = 2, BM = TG_BM, NT = TP_NT;
   constexpr int BSTR = BN + 2, L = (N - 1) / 2;
@@ -260,6 +264,115 @@ __global__ void __launch_bounds__(TP_THREADS, 3) k_tpipe(const TpParams P) {
       if (P.exp & 4) continue;
       if (!(P.exp & 1)) cta_wait_counter(gemm_done + (size_t)s * P.CT + ctl, P.nqg, tid);
       const double2* Tslot = P.T + (size_t)(s % P.nslot) * P.slot_elems + ctl * NT;
+      if constexpr (FV == 1) {
+        constexpr int R1 = smallest_prime_factor(N), R2 = N / R1;
+        static_assert(R1 * R2 == N && smallest_prime_factor(R2) == R2, "N must be a product of two primes");
+        double2* Ts = reinterpret_cast<double2*>(smem_raw);
+        const int col0 = ct * NT;
+        for (int k = 0; k < ncomp; ++k) {
+          const double2* src = Tslot + (size_t)(cl0 + k) * N * P.tpitch;
+          // first DIF stage (radix R1, twiddles) from L2 to shared memory
+          for (int item = tid; item < NT * R2; item += NTHR) {
+            const int c = item % NT, t = item / NT;
+            double xr[R1], xi[R1];
+#pragma unroll
+            for (int jj = 0; jj < R1; ++jj) {
+              const double2 v = __ldcg(src + (size_t)(t + jj * R2) * P.tpitch + c);
+              xr[jj] = v.x;
+              xi[jj] = v.y;
+            }
+            Radix<R1>::dft(xr, xi);
+            double2* base = Ts + t * NT + c;
+            base[0] = make_double2(xr[0], xi[0]);
+            if (t == 0) {
+#pragma unroll
+              for (int jj = 1; jj < R1; ++jj) base[jj * R2 * NT] = make_double2(xr[jj], xi[jj]);
+            } else {
+#pragma unroll
+              for (int jj = 1; jj < R1; ++jj) {
+                const double2 w = rou_s[t * jj];
+                base[jj * R2 * NT] = make_double2(xr[jj] * w.x - xi[jj] * w.y, xr[jj] * w.y + xi[jj] * w.x);
+              }
+            }
+          }
+          __syncthreads();
+          if (k + 1 == ncomp && tid == 0) {  // every T tile of the item has been read
+            __threadfence();
+            atomicAdd(fft_done + s, 1);
+          }
+          // last stage (radix R2) from shared memory to the volume rows, with the digest
+          const int comp = blk * BM + cl0 + k;
+          const CompRec rec = P.comps[comp];
+          const bool mir = P.mirror && rec.m > 0;
+          const long long sbit = (long long)0x8000000000000000ULL;
+          const long long mflip_r = (rec.m & 1) ? sbit : 0, mflip_i = (rec.m & 1) ? 0 : sbit;
+          double s2 = 0.0, pr = 0.0, pi = 0.0, ir = 0.0, ii = 0.0, g0r = 0.0, g0i = 0.0;
+          long long mx2 = 0;
+          for (int item = tid; item < NT * R1; item += NTHR) {
+            const int c = item % NT, bl = item / NT;
+            const int col = col0 + c;
+            if (col >= P.ncol) continue;
+            double xr[R2], xi[R2];
+            const double2* base = Ts + (size_t)(bl * R2) * NT + c;
+#pragma unroll
+            for (int jj = 0; jj < R2; ++jj) {
+              const double2 v = base[jj * NT];
+              xr[jj] = v.x;
+              xi[jj] = v.y;
+            }
+            double2* o = P.out + rec.slot * P.vol + col;
+            double2* om = mir ? P.out + rec.mslot * P.vol + col : nullptr;
+            const double qb = betaw_s[col / N];
+            double sr = 0.0, si = 0.0;
+            auto emit = [&](int jj, double vr, double vi) {
+              const int a = bl + R1 * jj;  // output frequency of position bl R2 + jj
+              const size_t idx = (size_t)a * P.rpitch;
+              __stcs(o + idx, make_double2(vr, vi));
+              if (om) {
+                const long long br = __double_as_longlong(vr) ^ mflip_r;
+                const long long bi = __double_as_longlong(vi) ^ mflip_i;
+                __stcs(om + idx, make_double2(__longlong_as_double(br), __longlong_as_double(bi)));
+              }
+              const double a2 = fma(vr, vr, vi * vi);
+              s2 += a2;
+              mx2 = max(mx2, __double_as_longlong(a2));
+              const double wgt = digest_weight((uint32_t)((size_t)a * P.ncol + col) * 0x9E3779B1u);
+              pr = fma(wgt, vr, pr);
+              pi = fma(wgt, vi, pi);
+              sr += vr;
+              si += vi;
+              if (a == 0 && col == 0) {
+                g0r = vr;
+                g0i = vi;
+              }
+            };
+            if constexpr (R2 >= kSinkMinRadix) {
+              Radix<R2>::dft_sink(xr, xi, emit);
+            } else {
+              Radix<R2>::dft(xr, xi);
+#pragma unroll
+              for (int jj = 0; jj < R2; ++jj) emit(jj, xr[jj], xi[jj]);
+            }
+            ir = fma(qb, sr, ir);
+            ii = fma(qb, si, ii);
+          }
+          double v[8] = {s2, __longlong_as_double(mx2), pr, pi, g0r, g0i, ir, ii};
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const double x = __shfl_down_sync(0xffffffffu, v[q], off);
+              v[q] = (q == 1) ? fmax(v[q], x) : v[q] + x;
+            }
+          if (lane == 0) {  // one partial per warp: k_digest adds them in a fixed order
+            double* part = P.partials + (((size_t)comp * P.n_tiles + ct) * (NTHR / 32) + warp) * 8;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) part[q] = v[q];
+          }
+          __syncthreads();  // the tile is rewritten by the next component's first stage
+        }
+        continue;
+      }
       double2* Tbuf = reinterpret_cast<double2*>(smem_raw);
       auto load_tile = [&](int k) {
         if (k < ncomp) {

@@ -486,6 +486,143 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// k_qfft_lean: the alpha pass of N = R1 R2 (49 = 7 x 7, 65 = 5 x 13) with two shared-memory
+// passes instead of six. The first DIF stage (radix R1, twiddles) reads its R1 rows of T
+// straight from global memory into registers and writes the tile once; after one barrier the
+// last stage (radix R2) reads its rows and its outputs go from registers to the volume rows
+// (and the mirror), with the digest accumulated on the way; one digest partial per warp
+// (4 per tile, reduced by k_digest in a fixed order). Same butterflies and twiddles as k_qfft:
+// the volumes are bitwise equal, the digest sums are associated differently. Less on-chip
+// traffic per sample, so less power under the HBM-bound T read.
+template <int N, int NT, int NTHR, int MINB>
+__global__ void __launch_bounds__(NTHR, MINB) k_qfft_lean(const QfParams P) {
+  constexpr int L = (N - 1) / 2;
+  constexpr int R1 = smallest_prime_factor(N), R2 = N / R1;
+  static_assert(R1 * R2 == N && smallest_prime_factor(R2) == R2, "N must be a product of two primes");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Ts = reinterpret_cast<double2*>(smem_raw);
+  double2* rou_s = Ts + N * NT;
+  double* betaw_s = reinterpret_cast<double*>(rou_s + N);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < N; i += NTHR) rou_s[i] = P.rou[i];
+  for (int i = tid; i <= L; i += NTHR) betaw_s[i] = P.betaw[i];
+  const int ct = blockIdx.x, comp = blockIdx.y;
+  const int col0 = ct * NT;
+  const double2* src = P.T + (size_t)comp * N * P.ncolp + col0;
+  // every thread's first-stage loads are issued before the table barrier
+  constexpr int ITEMS_A = (NT * R2 + NTHR - 1) / NTHR;
+  double xa[ITEMS_A][R1][2];
+#pragma unroll
+  for (int u = 0; u < ITEMS_A; ++u) {
+    const int item = tid + u * NTHR;
+    if (item < NT * R2) {
+      const int c = item % NT, t = item / NT;
+#pragma unroll
+      for (int jj = 0; jj < R1; ++jj) {
+        const double2 v = __ldcs(src + (size_t)(t + jj * R2) * P.ncolp + c);
+        xa[u][jj][0] = v.x;
+        xa[u][jj][1] = v.y;
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < ITEMS_A; ++u) {
+    const int item = tid + u * NTHR;
+    if (item < NT * R2) {
+      const int c = item % NT, t = item / NT;
+      double xr[R1], xi[R1];
+#pragma unroll
+      for (int jj = 0; jj < R1; ++jj) {
+        xr[jj] = xa[u][jj][0];
+        xi[jj] = xa[u][jj][1];
+      }
+      Radix<R1>::dft(xr, xi);
+      double2* base = Ts + t * NT + c;
+      base[0] = make_double2(xr[0], xi[0]);
+      if (t == 0) {
+#pragma unroll
+        for (int jj = 1; jj < R1; ++jj) base[jj * R2 * NT] = make_double2(xr[jj], xi[jj]);
+      } else {
+#pragma unroll
+        for (int jj = 1; jj < R1; ++jj) {
+          const double2 w = rou_s[t * jj];
+          base[jj * R2 * NT] = make_double2(xr[jj] * w.x - xi[jj] * w.y, xr[jj] * w.y + xi[jj] * w.x);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const CompRec rec = P.comps[comp];
+  const bool mir = P.mirror && rec.m > 0;
+  const long long sbit = (long long)0x8000000000000000ULL;
+  const long long mflip_r = (rec.m & 1) ? sbit : 0, mflip_i = (rec.m & 1) ? 0 : sbit;
+  double s2 = 0.0, pr = 0.0, pi = 0.0, ir = 0.0, ii = 0.0, g0r = 0.0, g0i = 0.0;
+  long long mx2 = 0;
+  for (int item = tid; item < NT * R1; item += NTHR) {
+    const int c = item % NT, bl = item / NT;
+    const int col = col0 + c;
+    if (col >= P.ncol) continue;
+    double xr[R2], xi[R2];
+    const double2* base = Ts + (size_t)(bl * R2) * NT + c;
+#pragma unroll
+    for (int jj = 0; jj < R2; ++jj) {
+      const double2 v = base[jj * NT];
+      xr[jj] = v.x;
+      xi[jj] = v.y;
+    }
+    double2* o = P.out + rec.slot * P.vol + col;
+    double2* om = mir ? P.out + rec.mslot * P.vol + col : nullptr;
+    const double qb = betaw_s[col / N];
+    double sr = 0.0, si = 0.0;
+    auto emit = [&](int jj, double vr, double vi) {
+      const int a = bl + R1 * jj;  // output frequency of position bl R2 + jj
+      const size_t idx = (size_t)a * P.rpitch;
+      __stcs(o + idx, make_double2(vr, vi));
+      if (om) {
+        const long long br = __double_as_longlong(vr) ^ mflip_r;
+        const long long bi = __double_as_longlong(vi) ^ mflip_i;
+        __stcs(om + idx, make_double2(__longlong_as_double(br), __longlong_as_double(bi)));
+      }
+      const double a2 = fma(vr, vr, vi * vi);
+      s2 += a2;
+      mx2 = max(mx2, __double_as_longlong(a2));
+      const double wgt = digest_weight((uint32_t)((size_t)a * P.ncol + col) * 0x9E3779B1u);
+      pr = fma(wgt, vr, pr);
+      pi = fma(wgt, vi, pi);
+      sr += vr;
+      si += vi;
+      if (a == 0 && col == 0) {
+        g0r = vr;
+        g0i = vi;
+      }
+    };
+    if constexpr (R2 >= kSinkMinRadix) {
+      Radix<R2>::dft_sink(xr, xi, emit);
+    } else {
+      Radix<R2>::dft(xr, xi);
+#pragma unroll
+      for (int jj = 0; jj < R2; ++jj) emit(jj, xr[jj], xi[jj]);
+    }
+    ir = fma(qb, sr, ir);
+    ii = fma(qb, si, ii);
+  }
+  double v[8] = {s2, __longlong_as_double(mx2), pr, pi, g0r, g0i, ir, ii};
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double x = __shfl_down_sync(0xffffffffu, v[q], off);
+      v[q] = (q == 1) ? fmax(v[q], x) : v[q] + x;
+    }
+  if (lane == 0) {
+    double* part = P.partials + (((size_t)comp * P.n_tiles + ct) * (NTHR / 32) + warp) * 8;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) part[q] = v[q];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // k_qfft_rt: the alpha pass for window band limits without a compile-time kernel and too
 // large for the single-pass runtime kernel's on-chip tile (n > 129, i.e. L_h >= 65 off the
 // BASELINE lengths): one component x NT columns per CTA, the n x NT tile of T in shared

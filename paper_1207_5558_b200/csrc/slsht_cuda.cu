@@ -151,6 +151,8 @@ struct slsht_cuda_plan {
   int tp_ct = 0, tp_ncg = 0, tp_nqg = 0, tp_nslot = 3, tp_fb = 8, tp_lag = 1;
   size_t tp_slot_elems = 0, tp_pipe_smem = 0;
   int tp_sync_ints = 0;
+  bool tp_lean = false;    //   k_qfft_lean (n = 49, 65): two smem passes, 4 digest partials per tile
+  int tp_pipe_fv = 0;      //   lean alpha pass with per-warp digest partials (4 per tile)
   int* d_tp_sync = nullptr;
   int* d_qg = nullptr;     //   k-step bounds of the q groups
   void (*tp_pipe_fn)(TpParams) = nullptr;
@@ -519,6 +521,14 @@ void build_plan(slsht_cuda_plan* p) {
   {
     const char* e = std::getenv("SLSHT_CUDA_TWO_PASS");
     p->use_tp = !(e && e[0] == '0') && tp_kernel(p->n, p->tp_fft, p->tp_threads, p->tp_nt);
+    if (const char* ln = std::getenv("SLSHT_CUDA_QFFT_LEAN")) {
+      const int mb = std::atoi(ln);  // CTAs per SM of the lean alpha pass (0: off)
+      if (p->use_tp && mb > 0 && (p->n == 49 || p->n == 65)) {
+        p->tp_lean = true;
+        if (p->n == 49) p->tp_fft = mb >= 8 ? k_qfft_lean<49, 32, 128, 8> : mb >= 6 ? k_qfft_lean<49, 32, 128, 6> : k_qfft_lean<49, 32, 128, 4>;
+        else p->tp_fft = mb >= 6 ? k_qfft_lean<65, 32, 128, 6> : mb >= 5 ? k_qfft_lean<65, 32, 128, 5> : k_qfft_lean<65, 32, 128, 4>;
+      }
+    }
     p->tp_ntiles = (p->ncol + p->tp_nt - 1) / p->tp_nt;
     // k_tgemm shape: <32, 2, 2, 3> (three 4-warp CTAs per SM, two stages) unless
     // SLSHT_CUDA_TGEMM selects <64, 2, 4, 1> (0), <32, 2, 3, 2> (1) or <32, 2, 4, 1> (2)
@@ -966,7 +976,9 @@ void build_plan(slsht_cuda_plan* p) {
         const char* e = std::getenv(name);
         return e ? std::atoi(e) : dflt;
       };
-      p->tp_pipe_fn = p->n == 49 ? k_tpipe<49> : k_tpipe<65>;
+      p->tp_pipe_fv = (env_int("SLSHT_CUDA_TP_FV", 0) || p->tp_lean) ? 1 : 0;
+      p->tp_pipe_fn = p->tp_pipe_fv ? (p->n == 49 ? k_tpipe<49, 1> : k_tpipe<65, 1>)
+                                    : (p->n == 49 ? k_tpipe<49, 0> : k_tpipe<65, 0>);
       const int nct = p->tp_ncolp / TP_BN;
       const size_t tile_bytes = (size_t)TG_BM * p->n * TP_BN * 16;
       int ct = env_int("SLSHT_CUDA_TP_CT", (int)std::max<size_t>(1, (20u << 20) / tile_bytes));
@@ -1010,7 +1022,7 @@ void build_plan(slsht_cuda_plan* p) {
                  "device output buffer does not fit in HBM (use the streaming ring mode)"};
   p->d_out = palloc<double2>(p, (size_t)p->n_slots * p->vstride);
   if (p->use_tp) p->d_T = palloc<double2>(p, t_bytes / 16);
-  const int parts_per_tile = p->use_fused ? FuCfg<49>::EPW : 1;
+  const int parts_per_tile = p->use_fused ? FuCfg<49>::EPW : ((p->tp_pipe && p->tp_pipe_fv) || p->tp_lean) ? TP_THREADS / 32 : 1;
   p->d_partials = palloc<double>(p, (size_t)p->max_chunk * p->n_col_tiles * parts_per_tile * 8);
   p->digest_rows = coeff_count(p->lmax);
   p->d_digest = palloc<double>(p, (size_t)p->digest_rows * 8);
@@ -1408,7 +1420,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     p->tp_fft<<<dim3(p->tp_ntiles, ch.count), p->tp_threads, p->tp_fft_smem, fs>>>(qf);
     CKL();
     if (overlap) {
-      k_digest<<<(ch.count + 3) / 4, 128, 0, fs>>>(comps, ch.count, p->n_col_tiles, p->n,
+      k_digest<<<(ch.count + 3) / 4, 128, 0, fs>>>(comps, ch.count, p->n_col_tiles * (p->tp_lean ? TP_THREADS / 32 : 1), p->n,
                                                     p->d_partials, p->mirror, p->d_digest);
       CKL();
       CK(cudaEventRecord(p->ev_fft[b], fs));
@@ -1428,6 +1440,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   k_digest<<<(ch.count + 3) / 4, 128, 0, s>>>(comps, ch.count,
                                                   p->use_lines   ? p->lines_nseg_dig
                                                   : p->use_fused ? p->n_col_tiles * FuCfg<49>::EPW
+                                                  : ((p->tp_pipe && p->tp_pipe_fv) || p->tp_lean) ? p->n_col_tiles * (TP_THREADS / 32)
                                                                  : p->n_col_tiles,
                                                   p->n, p->d_partials, p->mirror, p->d_digest);
   CKL();

@@ -1,6 +1,5 @@
-"""k_tpipe (SLSHT_CUDA_TP_PIPE=1) against the two-pass kernels over a degree range: time per
-call and bitwise equality of the digests.  python tools/pipe_check.py config l0 l1 [reps]
-Env: RING_MB (default 16384); SHAPES="ct,nqg,nslot,fb,lag;..." pipe shapes to try (0 = default)."""
+"""k_qfft_lean (SLSHT_CUDA_QFFT_LEAN=<CTAs per SM>) against k_qfft over a degree range: time per
+call and the largest digest difference.  python tools/lean_check.py config l0 l1 [reps]"""
 import os
 import sys
 
@@ -18,18 +17,14 @@ dev = torch.device("cuda:0")
 fd = torch.from_numpy(np.ascontiguousarray(f).view(np.float64)).to(dev)
 hd = torch.from_numpy(np.ascontiguousarray(h).view(np.float64)).to(dev)
 ring = int(os.environ.get("RING_MB", "16384")) << 20
-KEYS = ["SLSHT_CUDA_TP_CT", "SLSHT_CUDA_TP_NQG", "SLSHT_CUDA_TP_NSLOT", "SLSHT_CUDA_TP_FB", "SLSHT_CUDA_TP_LAG"]
 
 
 def run():
     dig = torch.zeros((S.coeff_count(cfg.L_g), 8), dtype=torch.float64, device=dev)
     with S.Plan(cfg.L_f, cfg.L_h, real_mode=cfg.real_mode, l_begin=l0, l_end=l1,
                 materialize=False, ring_bytes=ring) as p:
-        p.forward_device(fd.data_ptr(), hd.data_ptr(), inputs_on_device=True,
-                         digests_ptr=dig.data_ptr(), digests_on_device=True)
-        torch.cuda.synchronize()
         best = 1e30
-        for _ in range(reps):
+        for _ in range(reps + 1):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record()
@@ -42,20 +37,14 @@ def run():
         return best, p.computed_count, dig.cpu().numpy()
 
 
-os.environ["SLSHT_CUDA_TP_PIPE"] = "0"
+os.environ["SLSHT_CUDA_QFFT_LEAN"] = "0"
 ms0, comps, d0 = run()
-print(f"config {cfg_i} l in [{l0},{l1}): {comps} comps; two-pass {ms0:.3f} ms", flush=True)
+print(f"config {cfg_i} l in [{l0},{l1}): {comps} comps; k_qfft {ms0:.3f} ms", flush=True)
 r0, r1 = l0 * l0, l1 * l1
-os.environ["SLSHT_CUDA_TP_PIPE"] = "1"
-for shape in os.environ.get("SHAPES", "0,0,0,0,0").split(";"):
-    vals = [int(x) for x in shape.split(",")]
-    for k, v in zip(KEYS, vals):
-        if v:
-            os.environ[k] = str(v)
-        else:
-            os.environ.pop(k, None)
+for mb in os.environ.get("LEAN", "4,6,8").split(","):
+    os.environ["SLSHT_CUDA_QFFT_LEAN"] = mb
     ms, _, d1 = run()
     a, b = d0[r0:r1], d1[r0:r1]
     rel = float(np.max(np.abs(a - b) / np.maximum(np.max(np.abs(a), axis=0, keepdims=True), 1e-300)))
-    print(f"  pipe ct,nqg,nslot,fb,lag={shape}: {ms:.3f} ms ({ms / ms0:.3f}x), digests bitwise equal: "
-          f"{np.array_equal(a, b)}, max column-relative difference {rel:.2e}", flush=True)
+    print(f"  k_qfft_lean at {mb} CTAs per SM: {ms:.3f} ms ({ms / ms0:.3f}x), max column-relative "
+          f"digest difference {rel:.2e}", flush=True)

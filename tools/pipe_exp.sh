@@ -1,19 +1,10 @@
-SHAPES="13,16,3,4,1;13,16,4,4,2;10,16,4,4,2;10,16,4,4,1;7,16,6,4,2;10,12,4,4,2;10,16,4,8,2;10,16,5,4,3" timeout 300 python tools/pipe_check.py 4 300 400 2>&1
-for shape in "13 16 3 4 1" "10 16 4 4 2"; do
-  set -- $shape
-  echo "== full bench, pipe ct=$1 nqg=$2 nslot=$3 fb=$4 lag=$5"
-  SLSHT_CUDA_TP_PIPE=1 SLSHT_CUDA_TP_CT=$1 SLSHT_CUDA_TP_NQG=$2 SLSHT_CUDA_TP_NSLOT=$3 SLSHT_CUDA_TP_FB=$4 SLSHT_CUDA_TP_LAG=$5 timeout 600 python bench.py --no-cpu-baseline --steps 10 2>&1 | python -c "
-import json,sys
-for l in sys.stdin:
-    if l.startswith('{'):
-        d=json.loads(l); print(d['ms_per_step'], d['stages_ms'], d['clocks'], d['roundtrip_err'], d.get('digests_complete'))
-    else: print(l.rstrip()[:300])
-"
+for fv in 1 0; do
+echo "== FV=$fv"
+SLSHT_CUDA_TP_FV=$fv SHAPES="13,16,3,4,1;10,16,4,4,1;13,16,3,8,1;13,8,3,8,1" timeout 300 python tools/pipe_check.py 4 300 400 2>&1
+for e in 1 3; do
+  echo "== FV=$fv EXP=$e"
+  SLSHT_CUDA_TP_FV=$fv SLSHT_CUDA_TP_EXP=$e SHAPES="13,16,3,4,1;13,16,3,8,1" timeout 300 python tools/pipe_check.py 4 300 400 2>&1 | grep -v "^config"
 done
-echo "== full bench, two-pass"
-timeout 600 python bench.py --no-cpu-baseline --steps 10 2>&1 | python -c "
-import json,sys
-for l in sys.stdin:
-    if l.startswith('{'):
-        d=json.loads(l); print(d['ms_per_step'], d['stages_ms'], d['clocks'])
-"
+done
+echo "== config 3 (n = 65), FV=1"
+SHAPES="0,0,0,0,0;0,16,3,4,1;0,24,3,4,1" timeout 300 python tools/pipe_check.py 3 150 200 2>&1
