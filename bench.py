@@ -276,11 +276,14 @@ def host_sink_sample(S, C, cfg, f_np, h_np, dev: int, budget_bytes: float = 2.5e
         delivered, dropped = plan.forward_copy(f_np, h_np, out, first_index=l0 * l0)
         secs = time.perf_counter() - t0
     samples = delivered * cfg.volume
+    threads = int(os.environ.get("SLSHT_CUDA_HOST_THREADS", "0")) or min(16, os.cpu_count() or 1)
     return {"value": samples / secs, "unit": "samples/s", "gb_per_s": samples * 16 / secs / 1e9,
             "degrees": [l0, l1], "components": delivered, "dropped": dropped,
+            "host_copy_threads": threads,
             "how": ("slsht_cuda_forward + slsht_cuda_copy_sink into host memory (the "
-                    "materializing forward_fast's copy), degrees [l0, l1) of the config, wall "
-                    "clock, second call")}
+                    "materializing forward_fast's copy: disjoint rows, copied out of the pinned "
+                    "staging buffers by several host threads), degrees [l0, l1) of the config, "
+                    "wall clock, second call")}
 
 
 def run_ours(args) -> None:

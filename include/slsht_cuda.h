@@ -115,6 +115,18 @@ const char* slsht_cuda_last_error(const slsht_cuda_plan* plan);
 int slsht_cuda_forward(slsht_cuda_plan* plan, const double* f, const double* h,
                        slsht_host_sink sink, void* user);
 
+/* The materializing forward_fast(f, h, opts) (transform.hpp:164-165, transform.cpp:297-311:
+ * `components[coeff_index(l, m)] = volume`): the volume of every emitted (l, m) is copied to
+ * targets[coeff_index(l, m)] (volume_elems complex each; NULL entries and indices >= n_targets
+ * are skipped). The destinations are disjoint, so unlike the serialized sink of
+ * slsht_cuda_forward the copies out of the pinned staging buffers run on `threads` host
+ * threads (0: SLSHT_CUDA_HOST_THREADS, default min(16, cores)), divided over the devices of a
+ * multi-GPU plan. slsht_cuda_forward with slsht_cuda_copy_sink takes the same parallel path.
+ * delivered (may be NULL) receives the number of volumes copied. */
+int slsht_cuda_forward_scatter(slsht_cuda_plan* plan, const double* f, const double* h,
+                               double* const* targets, long long n_targets, int threads,
+                               long long* delivered);
+
 /* Device-consumer mode (the timed mode of bench.py). f, h are host pointers unless
  * inputs_on_device != 0. digests (may be NULL) receives coeff_count(lmax) x 8 doubles at
  * coeff_index(l, m) for every emitted component of the plan's shard (other rows untouched);

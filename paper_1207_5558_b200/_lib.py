@@ -25,6 +25,7 @@ EXPORTS = [
     "slsht_cuda_plan_destroy",
     "slsht_cuda_last_error",
     "slsht_cuda_forward",
+    "slsht_cuda_forward_scatter",
     "slsht_cuda_forward_device",
     "slsht_cuda_forward_capture",
     "slsht_cuda_device_output",
@@ -105,6 +106,9 @@ def load() -> C.CDLL:
     lib.slsht_cuda_last_error.restype = C.c_char_p
     lib.slsht_cuda_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.slsht_cuda_forward.restype = C.c_int
+    lib.slsht_cuda_forward_scatter.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                               C.c_longlong, C.c_int, C.POINTER(C.c_longlong)]
+    lib.slsht_cuda_forward_scatter.restype = C.c_int
     lib.slsht_cuda_forward_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                               C.c_void_p, C.c_int, C.c_int]
     lib.slsht_cuda_forward_device.restype = C.c_int

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -1607,6 +1608,9 @@ void run_group_device(slsht_cuda_plan* p, const double* f, const double* h, int 
   CK(cudaSetDevice(p->desc.device));
 }
 
+// tag passed as the sink of slsht_cuda_forward by slsht_cuda_forward_scatter (user = HostScatter)
+void scatter_marker(int, int, const double*, void*) {}
+
 struct LockedSink {
   slsht_host_sink sink;
   void* user;
@@ -1618,8 +1622,31 @@ void locked_sink(int l, int m, const double* vol, void* u) {
   s->sink(l, m, vol, s->user);
 }
 
+// Materializing delivery: every emitted volume is copied to its own destination (disjoint
+// rows), so the copies need no serialization and run on several host threads per chunk.
+struct HostScatter {
+  double* const* targets = nullptr;  // per coeff_index(l, m), or
+  double* base = nullptr;            // one array of rows (slsht_copy_target)
+  long long first_index = 0, count = 0;
+  int threads = 0;
+  std::atomic<long long> delivered{0}, dropped{0};
+  double* dest(int l, int m, long long vol) const {
+    const long long idx = (long long)coeff_index(l, m);
+    if (targets) return idx < count ? targets[idx] : nullptr;
+    const long long row = idx - first_index;
+    return (row >= 0 && row < count && base) ? base + 2 * row * vol : nullptr;
+  }
+};
+int host_threads(int asked) {
+  if (asked <= 0) {
+    if (const char* e = std::getenv("SLSHT_CUDA_HOST_THREADS")) asked = std::atoi(e);
+  }
+  if (asked <= 0) asked = (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+  return std::min(asked, 64);
+}
+
 void run_forward_sink(slsht_cuda_plan* p, const double* f, const double* h, slsht_host_sink sink,
-                      void* user);
+                      void* user, HostScatter* scatter = nullptr);
 void run_capture(slsht_cuda_plan* p, const double* f, const double* h, double* digests, int count,
                  const int* l, const int* m, const int* slot, double* volumes);
 
@@ -1770,7 +1797,7 @@ void run_capture(slsht_cuda_plan* p, const double* f, const double* h, double* d
 }
 
 void run_forward_sink(slsht_cuda_plan* p, const double* f, const double* h, slsht_host_sink sink,
-                      void* user) {
+                      void* user, HostScatter* scatter) {
   {
     if (p->materialize)
       throw Status{SLSHT_ERR_VALIDATION, "host-sink forward needs a streaming (ring) plan"};
@@ -1793,6 +1820,34 @@ void run_forward_sink(slsht_cuda_plan* p, const double* f, const double* h, slsh
       const Chunk& ch = p->chunks[ci];
       CK(cudaEventSynchronize(p->ev_copied[ch.buf]));
       const double2* base = p->h_stage[ch.buf];
+      if (scatter) {
+        // disjoint destinations: the chunk's volumes are copied by several host threads
+        const size_t vbytes = (size_t)p->vol * 16;
+        auto work = [&](int t, int nt) {
+          long long del = 0, drop = 0;
+          for (int k = t; k < ch.count; k += nt) {
+            const CompRec& r = p->comps[ch.comp0 + k];
+            for (int mir = 0; mir < (r.mslot >= 0 ? 2 : 1); ++mir) {
+              double* dst = scatter->dest(r.l, mir ? -r.m : r.m, p->vol);
+              if (!dst) {
+                ++drop;
+                continue;
+              }
+              std::memcpy(dst, base + (size_t)(mir ? p->max_chunk + k : k) * p->vol, vbytes);
+              ++del;
+            }
+          }
+          scatter->delivered += del;
+          scatter->dropped += drop;
+        };
+        const int nt = (int)std::max<long long>(
+            1, std::min<long long>(scatter->threads, (long long)ch.count * (long long)vbytes >> 20));
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t) pool.emplace_back(work, t, nt);
+        work(0, nt);
+        for (auto& th : pool) th.join();
+        return;
+      }
       for (int k = 0; k < ch.count; ++k) {
         const CompRec& r = p->comps[ch.comp0 + k];
         sink(r.l, r.m, reinterpret_cast<const double*>(base + (size_t)k * p->vol), user);
@@ -1880,8 +1935,31 @@ int slsht_cuda_forward(slsht_cuda_plan* p, const double* f, const double* h, sls
                        void* user) {
   if (!p) return SLSHT_ERR_VALIDATION;
   return guarded(p, [&] {
+    // the library's own copy sink writes disjoint rows: it is run as a parallel scatter
+    HostScatter sc;
+    HostScatter* scatter = nullptr;
+    slsht_copy_target* ct = nullptr;
+    if (sink == slsht_cuda_copy_sink && user) {
+      ct = static_cast<slsht_copy_target*>(user);
+      sc.base = ct->base;
+      sc.first_index = ct->first_index;
+      sc.count = ct->count;
+      sc.threads = host_threads(0);
+      scatter = &sc;
+    } else if (sink == scatter_marker && user) {
+      scatter = static_cast<HostScatter*>(user);
+    }
+    if (scatter && p->group())
+      scatter->threads = std::max(1, scatter->threads / (int)p->parts.size());
+    auto finish = [&] {
+      if (ct) {
+        ct->delivered += sc.delivered.load();
+        ct->dropped += sc.dropped.load();
+      }
+    };
     if (!p->group()) {
-      run_forward_sink(p, f, h, sink, user);
+      run_forward_sink(p, f, h, sink, user, scatter);
+      finish();
       return;
     }
     // one host thread per shard; sink calls serialized under one mutex (transform.cpp:282-284)
@@ -1894,7 +1972,7 @@ int slsht_cuda_forward(slsht_cuda_plan* p, const double* f, const double* h, sls
         slsht_cuda_plan* q = p->parts[k];
         try {
           CK(cudaSetDevice(q->desc.device));
-          run_forward_sink(q, f, h, locked_sink, &ls);
+          run_forward_sink(q, f, h, locked_sink, &ls, scatter);
         } catch (const Status& st) {
           errors[k] = st;
         } catch (const CudaError& e) {
@@ -1906,7 +1984,25 @@ int slsht_cuda_forward(slsht_cuda_plan* p, const double* f, const double* h, sls
     for (auto& t : pool) t.join();
     for (const Status& st : errors)
       if (st.code != SLSHT_OK) throw st;
+    finish();
   });
+}
+
+int slsht_cuda_forward_scatter(slsht_cuda_plan* p, const double* f, const double* h,
+                               double* const* targets, long long n_targets, int threads,
+                               long long* delivered) {
+  if (!p) return SLSHT_ERR_VALIDATION;
+  if (!targets || n_targets < 0) {
+    p->last_error = "null target table";
+    return SLSHT_ERR_VALIDATION;
+  }
+  HostScatter sc;
+  sc.targets = targets;
+  sc.count = n_targets;
+  sc.threads = host_threads(threads);
+  const int rc = slsht_cuda_forward(p, f, h, scatter_marker, &sc);
+  if (delivered) *delivered = sc.delivered.load();
+  return rc;
 }
 
 void slsht_cuda_copy_sink(int l, int m, const double* volume, void* target) {

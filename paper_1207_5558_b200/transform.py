@@ -269,6 +269,25 @@ class Plan:
         _raise(rc, self.handle)
         return int(tgt.delivered), int(tgt.dropped)
 
+    def forward_scatter(self, f: np.ndarray, h: np.ndarray, targets: dict, lmax: int,
+                        threads: int = 0) -> int:
+        """The materializing forward (slsht_cuda_forward_scatter): the volume of every emitted
+        (l, m) in `targets` ({(l, m): C-contiguous complex128 array of volume_elems}) is copied
+        into its array by several host threads. Returns the number of volumes copied."""
+        f = np.ascontiguousarray(f, np.complex128)
+        h = np.ascontiguousarray(h, np.complex128)
+        n = coeff_count(lmax)
+        table = (C.c_void_p * n)()
+        for (l, m), a in targets.items():
+            if a.dtype != np.complex128 or not a.flags.c_contiguous or a.size != self.volume_elems:
+                raise ValidationError("targets must be C-contiguous complex128 volumes")
+            table[coeff_index(l, m)] = a.ctypes.data
+        got = C.c_longlong(0)
+        rc = self.lib.slsht_cuda_forward_scatter(self.handle, _dptr(f), _dptr(h), table, n,
+                                                 int(threads), C.byref(got))
+        _raise(rc, self.handle)
+        return int(got.value)
+
 
 def _real_mode(f: SphCoeffs, h: SphCoeffs, opts: ForwardOptions) -> bool:
     # transform.cpp:253-254

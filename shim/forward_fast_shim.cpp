@@ -30,6 +30,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "slsht/errors.hpp"
@@ -173,6 +174,9 @@ void forward_fast(const SphCoeffs& f, const SphCoeffs& h, const ComponentSink& s
 }
 
 SlshtDistribution forward_fast(const SphCoeffs& f, const SphCoeffs& h, const ForwardOptions& opts) {
+  // transform.cpp:297-311. Every emitted volume is copied straight from the engine's pinned
+  // staging buffers into its So3Volume (slsht_cuda_forward_scatter: disjoint destinations,
+  // several host threads), instead of through the serialized sink and two more copies.
   SlshtDistribution dist;
   dist.L_f = f.band_limit;
   dist.L_h = h.band_limit;
@@ -182,8 +186,50 @@ SlshtDistribution forward_fast(const SphCoeffs& f, const SphCoeffs& h, const For
     throw ValidationError("fast engine computes components up to L_f + L_h only");
   dist.grid = so3_grid(dist.L_h);
   dist.components.assign(coeff_count(dist.lmax), So3Volume{});
-  forward_fast(
-      f, h, [&dist](int l, int m, const So3Volume& v) { dist.component(l, m) = v; }, opts);
+  const bool real_mode = opts.use_real_symmetry && f.real_signal && h.real_signal;
+  const PlanKey key{dist.L_f, dist.L_h, dist.lmax, real_mode, opts.emit_negative_m ? 1 : 0,
+                    static_cast<long long>(env_int("SLSHT_CUDA_RING_MB", 256)) << 20,
+                    device_list()};
+  // the components the call emits (transform.cpp:262-284): all (l, m) of l <= lmax, or in real
+  // mode m >= 0 and, with emit_negative_m, their mirrors; the others stay empty
+  std::vector<double*> targets(dist.components.size(), nullptr);
+  {
+    // allocation (first touch of every page) on several host threads, degree-interleaved
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int nt = std::max(1, std::min<int>({env_int("SLSHT_CUDA_HOST_THREADS", 16), (int)hw,
+                                              dist.lmax + 1}));
+    auto work = [&](int t) {
+      for (int l = t; l <= dist.lmax; l += nt)
+        for (int m = -l; m <= l; ++m) {
+          if (real_mode && m < 0 && !opts.emit_negative_m) continue;
+          So3Volume& v = dist.component(l, m);
+          v = So3Volume::zeros(dist.L_h);
+          targets[coeff_index(l, m)] = reinterpret_cast<double*>(v.values.data());
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+  }
+  std::lock_guard<std::mutex> lock(g_mutex);
+  bool owned = false;
+  slsht_cuda_plan* plan = acquire_plan(key, owned);
+  long long delivered = 0;
+  const int rc = slsht_cuda_forward_scatter(
+      plan, reinterpret_cast<const double*>(f.data.data()),
+      reinterpret_cast<const double*>(h.data.data()), targets.data(),
+      static_cast<long long>(targets.size()), 0, &delivered);
+  if (rc != SLSHT_OK) {
+    const std::string msg = slsht_cuda_last_error(plan);
+    if (rc == SLSHT_ERR_DEVICE && !owned)
+      g_plans.remove_if([plan](const auto& e) { return e.second == plan; });
+    if (owned || rc == SLSHT_ERR_DEVICE) slsht_cuda_plan_destroy(plan);
+    if (rc == SLSHT_ERR_VALIDATION) throw ValidationError(msg);
+    if (rc == SLSHT_ERR_NUMERIC) throw NumericError(msg);
+    throw std::runtime_error("slsht_cuda: " + msg);
+  }
+  if (owned) slsht_cuda_plan_destroy(plan);
   return dist;
 }
 
