@@ -35,6 +35,7 @@ struct TgParams {
   double2* T;            // [comp][n][ncolp]
   const short* qend;     // per k-step: T row (q mod n) completed by it, or -1
   int count, KP, ncolp, n;
+  int ustride;           // row stride of U (complex); KP may cover a sub-range of the rows
   int col_fast;          // 1: blockIdx.x = column tile (W L2-resident, U block read once)
   int t_stream;          // 1: T stored with the evict-first (.cs) hint
 };
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(tgemm_threads(BN, WNF, BM), MINB) k_tgemm(cons
         const int e = tid + j * TG_THREADS;
         const int c = e / TG_KS, k = e % TG_KS;
         const bool ok = comp0 + c < P.count && kb + k < P.KP;
-        cp_async16(Ad + c * TG_ASTR + k, P.U + (ok ? (size_t)(comp0 + c) * P.KP + kb + k : 0), ok);
+        cp_async16(Ad + c * TG_ASTR + k, P.U + (ok ? (size_t)(comp0 + c) * P.ustride + kb + k : 0), ok);
       }
 #pragma unroll
       for (int j = 0; j < TG_KS * BN / TG_THREADS; ++j) {
@@ -353,6 +354,13 @@ struct QfParams {
   const double* r43;  // k_r43_table (n = 129)
   FftPlan fft;        // k_qfft_rt: the runtime DIF plan (radices of n)
   int generic_dft;    // k_qfft_rt: n has a prime factor without a generated butterfly
+  // T rows [rc_lo, rc_hi) (the q of at most KC coupling terms, |q| > L - KC) are not stored by
+  // k_tgemm: k_qfft recomputes them from U and W (rc_k[r] terms from U row rc_urow[r])
+  const double2* U;
+  const double2* W;
+  int ustride, rc_lo, rc_hi;
+  short rc_urow[16];
+  signed char rc_k[16];
 };
 
 // row stride of the k_qfft tile: padded to == 2 (mod 8) for the DMMA radix-43 stage (n = 129)
@@ -382,12 +390,57 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
   const int ct = blockIdx.x, comp = blockIdx.y;
   const int col0 = ct * NT;
   {
+    // The rows k_tgemm left out (at most KC terms each, summed in increasing p). With
+    // 2 KC = NTHR / NT rows (KC = 2) every thread owns one (row, column): its operands are
+    // requested before the tile's copies and used after them, off the critical path.
+    const double2* Uc = P.U + (size_t)comp * P.ustride;
+    const bool rc_fast = N != 129 && (P.rc_hi - P.rc_lo) * NT == NTHR;
+    double2 fu0 = make_double2(0.0, 0.0), fu1 = fu0, fw0 = fu0, fw1 = fu0;
+    if (rc_fast) {
+      const int r = tid / NT, c = tid % NT;
+      const int urow = P.rc_urow[r];
+      const double2* wp = P.W + (size_t)urow * P.ncolp + col0 + c;
+      fu0 = __ldg(Uc + urow);
+      fw0 = __ldg(wp);
+      if (P.rc_k[r] > 1) {
+        fu1 = __ldg(Uc + urow + 1);
+        fw1 = __ldg(wp + P.ncolp);
+      }
+    }
     const double2* src = P.T + (size_t)comp * N * P.ncolp + col0;
     for (int e = tid; e < N * NT; e += NTHR) {
       const int row = e / NT, c = e % NT;
-      cp_async16(Ts + row * TS + c, src + (size_t)row * P.ncolp + c, true);
+      if (N == 129 || row < P.rc_lo || row >= P.rc_hi)  // (n = 129 stores every row)
+        cp_async16(Ts + row * TS + c, src + (size_t)row * P.ncolp + c, true);
     }
     cp_async_commit();
+    for (int e = tid; N != 129 && !rc_fast && e < (P.rc_hi - P.rc_lo) * NT; e += NTHR) {
+      const int r = e / NT, c = e % NT;
+      const int urow = P.rc_urow[r], K = P.rc_k[r];
+      const double2* wp = P.W + (size_t)urow * P.ncolp + col0 + c;
+      double ar = 0.0, ai = 0.0;
+      for (int k = 0; k < K; ++k) {
+        const double2 u = __ldg(Uc + urow + k);
+        const double2 w = __ldg(wp + (size_t)k * P.ncolp);
+        ar = fma(u.x, w.x, ar);
+        ar = fma(-u.y, w.y, ar);
+        ai = fma(u.x, w.y, ai);
+        ai = fma(u.y, w.x, ai);
+      }
+      Ts[(P.rc_lo + r) * TS + c] = make_double2(ar, ai);
+    }
+    if (rc_fast) {  // (u1 = w1 = 0 for a one-term row: the same fma sequence, exact)
+      double ar = 0.0, ai = 0.0;
+      ar = fma(fu0.x, fw0.x, ar);
+      ar = fma(-fu0.y, fw0.y, ar);
+      ai = fma(fu0.x, fw0.y, ai);
+      ai = fma(fu0.y, fw0.x, ai);
+      ar = fma(fu1.x, fw1.x, ar);
+      ar = fma(-fu1.y, fw1.y, ar);
+      ai = fma(fu1.x, fw1.y, ai);
+      ai = fma(fu1.y, fw1.x, ai);
+      Ts[(P.rc_lo + tid / NT) * TS + tid % NT] = make_double2(ar, ai);
+    }
   }
   cp_async_wait<0>();
   __syncthreads();

@@ -152,6 +152,11 @@ struct slsht_cuda_plan {
   int tp_ct = 0, tp_ncg = 0, tp_nqg = 0, tp_nslot = 3, tp_fb = 8, tp_lag = 1;
   size_t tp_slot_elems = 0, tp_pipe_smem = 0;
   int tp_sync_ints = 0;
+  int tp_kc = 0;           //   T rows of at most tp_kc coupling terms are recomputed by k_qfft
+  int tp_ks_lo = 0;        //   first k-step of k_tgemm's row range
+  int tp_KPsub = 0;        //   rows of k_tgemm's range (whole stages)
+  short tp_rc_urow[16] = {};
+  signed char tp_rc_k[16] = {};
   bool tp_lean = false;    //   k_qfft_lean (n = 49, 65): two smem passes, 4 digest partials per tile
   int tp_pipe_fv = 0;      //   lean alpha pass with per-warp digest partials (4 per tile)
   int* d_tp_sync = nullptr;
@@ -757,6 +762,40 @@ void build_plan(slsht_cuda_plan* p) {
       qend[urb[jq + 1] / 4 - 1] = (short)(jq >= L ? jq - L : jq + L + 1);
     }
     p->ws_stages.group_elems = rows_pad;
+    // The q of few coupling terms (|q| > L - KC: K_q = L + 1 - |q| <= KC, the first and last KC
+    // q of the q-major order) cost k_tgemm a whole k-step each and the T round trip 2 KC of n
+    // rows; k_qfft recomputes them from U and W instead (n = 49, 65; not with the pipeline or
+    // the lean alpha pass, which read every T row). SLSHT_CUDA_TP_KC=0..8 sets KC; with KC = 2
+    // every k_qfft thread owns one recomputed (row, column) and requests its operands ahead of
+    // the tile (config 4: k_tgemm 74.7 -> 70.8 ms, k_qfft +1 ms; KC = 4: slower, the W rows of
+    // the recomputation are L2 traffic per (component, column tile)).
+    p->tp_KPsub = p->tp_KP;
+    {
+      const char* pe = std::getenv("SLSHT_CUDA_TP_PIPE");
+      const bool pipe_req = pe && pe[0] == '1';
+      int kc = (p->n == 49 || p->n == 65) && !pipe_req && !p->tp_lean ? 2 : 0;  // measured best
+      if (const char* e = std::getenv("SLSHT_CUDA_TP_KC")) kc = std::atoi(e);
+      if (!(p->n == 49 || p->n == 65) || pipe_req || p->tp_lean) kc = 0;
+      kc = std::max(0, std::min({kc, 8, L}));
+      if (kc > 0) {
+        const int ks_lo = urb[kc] / 4, ks_hi = urb[p->n - kc] / 4;
+        std::vector<short> sub(qend.begin() + ks_lo, qend.begin() + ks_hi);
+        while (sub.size() % (TG_KS / 4)) sub.push_back((short)-1);
+        // the padding k-steps read the rows that follow (never stored): they must exist
+        if ((int)sub.size() * 4 + ks_lo * 4 <= p->tp_KP) {
+          p->tp_kc = kc;
+          p->tp_ks_lo = ks_lo;
+          p->tp_KPsub = (int)sub.size() * 4;
+          qend = sub;
+          for (int r = 0; r < 2 * kc; ++r) {
+            const int trow = L + 1 - kc + r;          // T row = q mod n
+            const int q = trow <= L ? trow : trow - p->n;
+            p->tp_rc_urow[r] = (short)urb[q + L];
+            p->tp_rc_k[r] = (signed char)(L + 1 - std::abs(q));
+          }
+        }
+      }
+    }
   }
   // ---- fused layout (k_fused, kernels_fused.cuh): T rows r = q mod n in G row groups
   // (rows j + G k); each group's sequence of k-steps (its rows in order, every row padded to
@@ -1358,12 +1397,13 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     const int b = overlap ? ch.buf : 0;
     if (overlap && p->fft_rec[b]) CK(cudaStreamWaitEvent(s, p->ev_fft[b], 0));
     TgParams tg{};
-    tg.U = p->d_U;
-    tg.W = p->d_W;
+    tg.U = p->d_U + 4 * p->tp_ks_lo;
+    tg.W = p->d_W + (size_t)4 * p->tp_ks_lo * p->tp_ncolp;
+    tg.ustride = p->tp_KP;
     tg.T = p->d_T + b * p->tp_t_elems;
     tg.qend = p->d_qend;
     tg.count = ch.count;
-    tg.KP = p->tp_KP;
+    tg.KP = p->tp_KPsub;
     tg.ncolp = p->tp_ncolp;
     tg.n = p->n;
     const int tbm = tgemm_variant(p->tp_gv).bm;
@@ -1418,6 +1458,15 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     qf.r43 = p->d_r43;
     qf.fft = p->fft;
     qf.generic_dft = p->generic_dft;
+    qf.U = p->d_U;
+    qf.W = p->d_W;
+    qf.ustride = p->tp_KP;
+    qf.rc_lo = p->tp_kc ? p->L_h + 1 - p->tp_kc : 0;
+    qf.rc_hi = p->tp_kc ? p->L_h + 1 + p->tp_kc : 0;
+    for (int r = 0; r < 16; ++r) {
+      qf.rc_urow[r] = p->tp_rc_urow[r];
+      qf.rc_k[r] = p->tp_rc_k[r];
+    }
     p->tp_fft<<<dim3(p->tp_ntiles, ch.count), p->tp_threads, p->tp_fft_smem, fs>>>(qf);
     CKL();
     if (overlap) {
