@@ -37,7 +37,7 @@ struct TgParams {
   int count, KP, ncolp, n;
   int ustride;           // row stride of U (complex); KP may cover a sub-range of the rows
   int col_fast;          // 1: blockIdx.x = column tile (W L2-resident, U block read once)
-  int t_stream;          // 1: T stored with the evict-first (.cs) hint
+  int t_stream;          // 1: T stored with the evict-first (.cs) hint; 2: timing experiment, no T stores
 };
 
 __host__ __device__ constexpr int tgemm_threads(int BN, int WNF, int BM = TG_BM) {
@@ -123,6 +123,9 @@ __global__ void __launch_bounds__(tgemm_threads(BN, WNF, BM), MINB) k_tgemm(cons
   reset();
   const int scomp = comp0 + wm * 32 + (lane >> 2);
   const int scol = col0 + wn * 8 * WNF + 2 * (lane & 3);
+  // T address of the thread's first component row; rows mi 8 further are tstep elements on
+  double2* const tbase = P.T + (size_t)scomp * P.n * P.ncolp + scol;
+  const size_t tstep = (size_t)8 * P.n * P.ncolp;
 
   for (int st = 0; st < nst; ++st) {
     cp_async_wait<TG_NST - 2>();
@@ -164,11 +167,11 @@ __global__ void __launch_bounds__(tgemm_threads(BN, WNF, BM), MINB) k_tgemm(cons
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
           const int comp = scomp + mi * 8;
-          if (comp < P.count) {
-            double2* dst = P.T + ((size_t)comp * P.n + row) * P.ncolp + scol;
+          if (comp < P.count && P.t_stream != 2) {
+            double2* dst = tbase + (size_t)mi * tstep + row * P.ncolp;
 #pragma unroll
             for (int ni = 0; ni < WNF; ++ni) {  // 32 B per lane: 4 lanes write one whole 128-B line
-              if (P.t_stream)
+              if (P.t_stream == 1)
                 st_global_cs_v4(dst + ni * 8, c1[mi][ni][0] - c3[mi][ni][0],
                                 c1[mi][ni][0] + c2[mi][ni][0], c1[mi][ni][1] - c3[mi][ni][1],
                                 c1[mi][ni][1] + c2[mi][ni][1]);

@@ -145,7 +145,7 @@ struct slsht_cuda_plan {
   bool use_fused = false;  // fused coupling (k_fused, n = 49): GEMM + FFT + epilogue in one
   int fu_KP = 0, fu_upad = 0;
   bool tp_col_fast = false; //  k_tgemm raster: column tiles fastest (W L2-resident)
-  bool tp_t_stream = false; //  k_tgemm: T stores with the evict-first hint
+  int tp_t_stream = 0;      //  k_tgemm: 1 T stores with the evict-first hint; 2 no T stores (timing)
   size_t tp_t_elems = 0;   //   one T buffer (two in the overlapped schedule)
   bool tp_pipe = false;    //   k_tpipe: GEMM and alpha-pass items in one persistent kernel over an
                            //   L2-resident ring of T slots (kernels_tpipe.cuh; n = 49, 65)
@@ -751,7 +751,7 @@ void build_plan(slsht_cuda_plan* p) {
     // chunk's U is read from HBM once (SLSHT_CUDA_TG_RASTER=0/1 forces either order)
     p->tp_col_fast = (size_t)p->tp_KP * p->tp_ncolp * 16 <= (48u << 20);
     if (const char* e = std::getenv("SLSHT_CUDA_TG_RASTER")) p->tp_col_fast = e[0] == '1';
-    if (const char* e = std::getenv("SLSHT_CUDA_TG_STREAM")) p->tp_t_stream = e[0] == '1';
+    if (const char* e = std::getenv("SLSHT_CUDA_TG_STREAM")) p->tp_t_stream = std::atoi(e);
     qend.assign(rows_pad / 4, (short)-1);
     for (int jq = 0; jq < p->n; ++jq) {
       for (int c = qoff[jq]; c < qoff[jq + 1]; ++c) {
@@ -1408,7 +1408,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     tg.n = p->n;
     const int tbm = tgemm_variant(p->tp_gv).bm;
     tg.col_fast = p->tp_col_fast ? 1 : 0;
-    tg.t_stream = p->tp_t_stream ? 1 : 0;
+    tg.t_stream = p->tp_t_stream;
     const int nbm = (ch.count + tbm - 1) / tbm, nbn = p->tp_ncolp / p->tp_bn;
     const dim3 tgrid(tg.col_fast ? nbn : nbm, tg.col_fast ? nbm : nbn);
     if (p->tp_gv == 2) {
