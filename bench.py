@@ -461,7 +461,10 @@ def run_ours(args) -> None:
         comps = plan.computed_count
         gemm_flops = 8.0 * comps * (cfg.L_h + 1) ** 2 * n * nb  # complex MACs x 8 (canonical)
         tg_ms, qf_ms = stage_ms[3], stage_ms[5]
-        t_bytes = 16.0 * comps * n * n * nb
+        # T rows k_qfft recomputes instead of reading (SLSHT_CUDA_TP_KC, default 2 at n = 49, 65)
+        kc = int(os.environ.get("SLSHT_CUDA_TP_KC", "2" if n in (49, 65) else "0"))
+        kc = kc if n in (49, 65) else 0
+        t_bytes = 16.0 * comps * (n - 2 * kc) * n * nb
         tg = {"bound": "tensor", "kernel": "k_tgemm (coupling GEMM on the FP64 tensor cores)",
               "achieved": gemm_flops / (tg_ms / 1e3) / 1e12, "peak": P_FP64_TFLOPS,
               "unit": "TFLOP/s", "frac": gemm_flops / (tg_ms / 1e3) / 1e12 / P_FP64_TFLOPS,

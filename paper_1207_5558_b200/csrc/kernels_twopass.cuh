@@ -411,10 +411,15 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
       }
     }
     const double2* src = P.T + (size_t)comp * N * P.ncolp + col0;
-    for (int e = tid; e < N * NT; e += NTHR) {
+    // rows [0, rc_lo) and [rc_hi, N): two plain loops (rc_lo = rc_hi = 0 when every row is stored)
+    const int e_lo = N == 129 ? 0 : P.rc_lo * NT, e_hi = N == 129 ? 0 : P.rc_hi * NT;
+    for (int e = tid; e < e_lo; e += NTHR) {
       const int row = e / NT, c = e % NT;
-      if (N == 129 || row < P.rc_lo || row >= P.rc_hi)  // (n = 129 stores every row)
-        cp_async16(Ts + row * TS + c, src + (size_t)row * P.ncolp + c, true);
+      cp_async16(Ts + row * TS + c, src + (size_t)row * P.ncolp + c, true);
+    }
+    for (int e = e_hi + tid; e < N * NT; e += NTHR) {
+      const int row = e / NT, c = e % NT;
+      cp_async16(Ts + row * TS + c, src + (size_t)row * P.ncolp + c, true);
     }
     cp_async_commit();
     for (int e = tid; N != 129 && !rc_fast && e < (P.rc_hi - P.rc_lo) * NT; e += NTHR) {
