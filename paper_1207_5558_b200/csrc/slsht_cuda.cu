@@ -19,6 +19,7 @@
 #include "kernels_couple.cuh"
 #include "kernels_couple_ws.cuh"
 #include "kernels_couple_lines.cuh"
+#include "kernels_couple_reg.cuh"
 #include "kernels_twopass.cuh"
 #include "kernels_tpipe.cuh"
 #include "kernels_fused.cuh"
@@ -121,6 +122,7 @@ struct slsht_cuda_plan {
   int generic_dft = 0;
   size_t couple_smem = 0;
   bool use_ws = false;  // warp-specialized persistent coupling kernel for this length
+  bool use_reg = false; // thread-per-column register kernel (k_couple_reg, n = 17)
   WsKernel ws{};
   WsStages ws_stages{};
   int num_sms = 0;
@@ -486,6 +488,8 @@ void set_func_attributes(const slsht_cuda_plan* p) {
     opt(tgemm_variant(p->tp_gv).fn, p->tp_gemm_smem);
     opt(p->tp_fft, p->tp_fft_smem);
     if (p->tp_pipe) opt(p->tp_pipe_fn, p->tp_pipe_smem);
+  } else if (p->use_reg) {
+    opt(k_couple_reg<17>, p->couple_smem);
   } else if (p->use_ws) {
     opt(p->ws.fn, p->couple_smem);
   } else {
@@ -632,6 +636,12 @@ void build_plan(slsht_cuda_plan* p) {
     p->lines_threads = LnCfg<33>::NTHREADS;
     p->couple_smem = LnCfg<33>::SMEM;
     p->lines_upad = LnCfg<33>::UPAD;
+  } else if (p->n == 17 && !(std::getenv("SLSHT_CUDA_REG") && std::getenv("SLSHT_CUDA_REG")[0] == '0') &&
+             std::getenv("SLSHT_CUDA_NO_WS") == nullptr) {
+    // n = 17 (L_h = 8, config 1): one thread per (component, column), all in registers
+    p->use_reg = true;
+    p->MG = 1;
+    p->NG = RG_NT / 8;  // 32-column tiles
   } else if (std::getenv("SLSHT_CUDA_NO_WS") == nullptr && ws_kernel(p->n, p->ws)) {
     p->use_ws = true;
     p->MG = p->ws.MT / 8;
@@ -1096,6 +1106,8 @@ void build_plan(slsht_cuda_plan* p) {
         CK(cudaEventCreateWithFlags(&p->ev_fft[i], cudaEventDisableTiming));
       }
     }
+  } else if (p->use_reg) {
+    p->couple_smem = couple_reg_smem_bytes(p->n);
   } else if (p->use_ws) {
     p->couple_smem = p->ws.smem;
   } else {
@@ -1314,6 +1326,19 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
       }
     }
 #endif
+  } else if (p->use_reg) {
+    RegParams rp{};
+    rp.c = prm;
+    rp.n_tiles = p->n_col_tiles;
+    // components per CTA: one wave of two CTAs per SM when the chunk allows (each CTA stages its W
+    // tile once), 8..256
+    {
+      const int groups = std::max(1, 2 * p->num_sms / std::max(1, p->n_col_tiles));
+      rp.cpb = std::min(256, std::max(8, (ch.count + groups - 1) / groups));
+      if (const char* e = std::getenv("SLSHT_CUDA_REG_CPB")) rp.cpb = std::max(1, std::atoi(e));
+    }
+    const dim3 grid(p->n_col_tiles, (ch.count + rp.cpb - 1) / rp.cpb);
+    k_couple_reg<17><<<grid, RG_THREADS, p->couple_smem, s>>>(rp);
   } else if (p->use_ws) {
     WsParams wp{};
     wp.c = prm;

@@ -4,7 +4,7 @@ With SLSHT_CUDA_GUARD=1 every plan-owned device buffer gets 64-KB guard bands (p
 on both sides, verified after every call (a DeviceError names the buffer and the byte); the
 GPU test tests/test_gpu.py::test_guard_bands_every_kernel runs these cases that way and checks
 the results bitwise against unguarded plans. (compute-sanitizer is closed on this GPU pool.)
-Cases: n = 17 (k_couple_ws), 33 (k_couple_lines), 49 (k_tgemm + k_qfft<49>; k_fused with
+Cases: n = 17 (k_couple_reg; k_couple_ws with SLSHT_CUDA_REG=0), 33 (k_couple_lines), 49 (k_tgemm + k_qfft<49>; k_fused with
 SLSHT_CUDA_FUSED=1; k_tpipe and k_qfft_lean with their knobs), 65 (k_qfft<65>), 129 (k_qfft<129>, DMMA radix-43), 225 (k_qfft_rt),
 21 (runtime-plan k_couple<0>), and with them the setup kernels (k_glnodes, k_setup_main,
 k_delta, k_dtab, k_wtab), k_agen, k_modgemm, k_digest, k_inverse."""
@@ -17,7 +17,8 @@ sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 import paper_1207_5558_b200 as S  # noqa: E402
 
 CASES = [  # (L_f, L_h, real_mode, lmax, engine knobs)
-    (6, 8, False, 8, {}),     # n = 17
+    (6, 8, False, 8, {}),     # n = 17 (k_couple_reg)
+    (6, 8, True, 8, {"SLSHT_CUDA_REG": "0"}),   # n = 17 on k_couple_ws
     (4, 16, True, 10, {}),    # n = 33, real mode (mirrors)
     (3, 24, False, 6, {}),    # n = 49 two-pass
     (3, 24, False, 6, {"SLSHT_CUDA_FUSED": "1"}),     # n = 49 fused
