@@ -48,15 +48,15 @@ __global__ void __launch_bounds__(RG_THREADS, 2) k_couple_reg(const RegParams R)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ct = blockIdx.x, col0 = ct * RG_NT, col = col0 + lane;
   const bool ok = col < P.ncol;
+  // the W tile: asynchronous copies (zero fill past the last column), all in flight at once
   for (int e = tid; e < NPQ * RG_NT; e += RG_THREADS) {
     const int c = e / RG_NT, k = e % RG_NT;
-    Ws[e] = col0 + k < P.ncol ? P.W[(size_t)c * P.ncol + col0 + k] : make_double2(0.0, 0.0);
+    const bool in = col0 + k < P.ncol;
+    cp_async16(Ws + e, P.W + (in ? (size_t)c * P.ncol + col0 + k : 0), in);
   }
+  cp_async_commit();
   for (int i = tid; i <= L; i += RG_THREADS) betaw_s[i] = P.betaw[i];
-  __syncthreads();
-  const double qb = ok ? betaw_s[col / N] : 0.0;
   const long long sbit = (long long)0x8000000000000000ULL;
-
   const int comp_end = min(P.count, (int)(blockIdx.y + 1) * R.cpb);
   // the warp's U rows: copied asynchronously one component ahead (two buffers per warp)
   double2* Uw = Us + warp * 2 * NPQ;
@@ -66,6 +66,9 @@ __global__ void __launch_bounds__(RG_THREADS, 2) k_couple_reg(const RegParams R)
     cp_async_commit();
   };
   load_u(blockIdx.y * R.cpb + warp, 0);
+  cp_async_wait<1>();  // this thread's part of the W tile
+  __syncthreads();
+  const double qb = ok ? betaw_s[col / N] : 0.0;
   int buf = 0;
   for (int comp = blockIdx.y * R.cpb + warp; comp < comp_end; comp += RG_WARPS, buf ^= 1) {
     load_u(comp + RG_WARPS, buf ^ 1);
@@ -79,18 +82,18 @@ __global__ void __launch_bounds__(RG_THREADS, 2) k_couple_reg(const RegParams R)
 #pragma unroll
       for (int jq = 0; jq < N; ++jq) {
         const int q = jq - L, K = L + 1 - (q < 0 ? -q : q);
-        double ar = 0.0, ai = 0.0;
+        double arx = 0.0, ary = 0.0, aix = 0.0, aiy = 0.0;  // four independent chains per row
 #pragma unroll
         for (int k = 0; k < K; ++k, ++c) {
           const double2 u = Uc[c];  // broadcast
           const double2 w = Ws[c * RG_NT + lane];
-          ar = fma(u.x, w.x, ar);
-          ar = fma(-u.y, w.y, ar);
-          ai = fma(u.x, w.y, ai);
-          ai = fma(u.y, w.x, ai);
+          arx = fma(u.x, w.x, arx);
+          ary = fma(u.y, w.y, ary);
+          aix = fma(u.x, w.y, aix);
+          aiy = fma(u.y, w.x, aiy);
         }
-        xr[q < 0 ? q + N : q] = ar;
-        xi[q < 0 ? q + N : q] = ai;
+        xr[q < 0 ? q + N : q] = arx - ary;
+        xi[q < 0 ? q + N : q] = aix + aiy;
       }
     }
     Radix<N>::dft(xr, xi);  // a prime length: outputs in natural order (the identity permutation)
