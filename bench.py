@@ -499,7 +499,10 @@ def run_ours(args) -> None:
             src = "CUDA events on the engine stream, two profiled steps after the timed ones"
         achieved = alg_bytes / (couple_ms / 1e3) / 1e9
         roofline = {
-            "bound": "hbm", "kernel": "k_couple (coupling DMMA + alpha FFT + store/digest epilogue)",
+            "bound": "hbm",
+            "kernel": {17: "k_couple_reg (coupling on FP64 FMAs + radix-17 alpha DFT + store/digest epilogue, in registers)",
+                       33: "k_couple_lines (coupling DMMA + alpha FFT + line-aligned store/digest epilogue)"}.get(
+                2 * cfg.L_h + 1, "k_couple (coupling DMMA + alpha FFT + store/digest epilogue)"),
             "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
             "peak_source": peaks["source"], "algorithmic_bytes_per_step": alg_bytes,
