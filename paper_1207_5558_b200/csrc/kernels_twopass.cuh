@@ -393,23 +393,11 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
   const int ct = blockIdx.x, comp = blockIdx.y;
   const int col0 = ct * NT;
   {
-    // The rows k_tgemm left out (at most KC terms each, summed in increasing p). With
-    // 2 KC = NTHR / NT rows (KC = 2) every thread owns one (row, column): its operands are
-    // requested before the tile's copies and used after them, off the critical path.
+    // The rows k_tgemm left out (at most KC terms each, summed in increasing p). With KC = 2 or 4
+    // every thread owns KC / 2 (row, column) items (rows g and g + 4 of a thread group g pair a
+    // long row with a short one): their operands are requested right after the tile's copies,
+    // all at once, and used when they arrive; the general loop serves the other KC.
     const double2* Uc = P.U + (size_t)comp * P.ustride;
-    const bool rc_fast = N != 129 && (P.rc_hi - P.rc_lo) * NT == NTHR;
-    double2 fu0 = make_double2(0.0, 0.0), fu1 = fu0, fw0 = fu0, fw1 = fu0;
-    if (rc_fast) {
-      const int r = tid / NT, c = tid % NT;
-      const int urow = P.rc_urow[r];
-      const double2* wp = P.W + (size_t)urow * P.ncolp + col0 + c;
-      fu0 = __ldg(Uc + urow);
-      fw0 = __ldg(wp);
-      if (P.rc_k[r] > 1) {
-        fu1 = __ldg(Uc + urow + 1);
-        fw1 = __ldg(wp + P.ncolp);
-      }
-    }
     const double2* src = P.T + (size_t)comp * N * P.ncolp + col0;
     // rows [0, rc_lo) and [rc_hi, N): two plain loops (rc_lo = rc_hi = 0 when every row is stored)
     const int e_lo = N == 129 ? 0 : P.rc_lo * NT, e_hi = N == 129 ? 0 : P.rc_hi * NT;
@@ -422,32 +410,61 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
       cp_async16(Ts + row * TS + c, src + (size_t)row * P.ncolp + c, true);
     }
     cp_async_commit();
-    for (int e = tid; N != 129 && !rc_fast && e < (P.rc_hi - P.rc_lo) * NT; e += NTHR) {
-      const int r = e / NT, c = e % NT;
-      const int urow = P.rc_urow[r], K = P.rc_k[r];
-      const double2* wp = P.W + (size_t)urow * P.ncolp + col0 + c;
-      double ar = 0.0, ai = 0.0;
-      for (int k = 0; k < K; ++k) {
-        const double2 u = __ldg(Uc + urow + k);
-        const double2 w = __ldg(wp + (size_t)k * P.ncolp);
-        ar = fma(u.x, w.x, ar);
-        ar = fma(-u.y, w.y, ar);
-        ai = fma(u.x, w.y, ai);
-        ai = fma(u.y, w.x, ai);
+    if constexpr (N != 129) {
+      constexpr int GR = NTHR / NT;  // rows per item round
+      const int nrc = P.rc_hi - P.rc_lo;
+      auto owned = [&](auto it_tag) {
+        constexpr int IT = decltype(it_tag)::value, MAXK = 2 * IT;
+        double2 fu[IT][MAXK], fw[IT][MAXK];
+        const int c = tid % NT;
+#pragma unroll
+        for (int i = 0; i < IT; ++i) {
+          const int r = tid / NT + i * GR;
+          const int urow = P.rc_urow[r], K = P.rc_k[r];
+          const double2* wp = P.W + (size_t)urow * P.ncolp + col0 + c;
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k) {
+            fu[i][k] = fw[i][k] = make_double2(0.0, 0.0);
+            if (k < K) {
+              fu[i][k] = __ldg(Uc + urow + k);
+              fw[i][k] = __ldg(wp + (size_t)k * P.ncolp);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < IT; ++i) {  // (absent terms are zeros: exact)
+          double ar = 0.0, ai = 0.0;
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k) {
+            ar = fma(fu[i][k].x, fw[i][k].x, ar);
+            ar = fma(-fu[i][k].y, fw[i][k].y, ar);
+            ai = fma(fu[i][k].x, fw[i][k].y, ai);
+            ai = fma(fu[i][k].y, fw[i][k].x, ai);
+          }
+          Ts[(P.rc_lo + tid / NT + i * GR) * TS + c] = make_double2(ar, ai);
+        }
+      };
+      if (nrc == GR) {
+        owned(std::integral_constant<int, 1>{});
+      } else if (nrc == 2 * GR) {
+        owned(std::integral_constant<int, 2>{});
+      } else {
+        for (int e = tid; e < nrc * NT; e += NTHR) {
+          const int r = e / NT, c = e % NT;
+          const int urow = P.rc_urow[r], K = P.rc_k[r];
+          const double2* wp = P.W + (size_t)urow * P.ncolp + col0 + c;
+          double ar = 0.0, ai = 0.0;
+          for (int k = 0; k < K; ++k) {
+            const double2 u = __ldg(Uc + urow + k);
+            const double2 w = __ldg(wp + (size_t)k * P.ncolp);
+            ar = fma(u.x, w.x, ar);
+            ar = fma(-u.y, w.y, ar);
+            ai = fma(u.x, w.y, ai);
+            ai = fma(u.y, w.x, ai);
+          }
+          Ts[(P.rc_lo + r) * TS + c] = make_double2(ar, ai);
+        }
       }
-      Ts[(P.rc_lo + r) * TS + c] = make_double2(ar, ai);
-    }
-    if (rc_fast) {  // (u1 = w1 = 0 for a one-term row: the same fma sequence, exact)
-      double ar = 0.0, ai = 0.0;
-      ar = fma(fu0.x, fw0.x, ar);
-      ar = fma(-fu0.y, fw0.y, ar);
-      ai = fma(fu0.x, fw0.y, ai);
-      ai = fma(fu0.y, fw0.x, ai);
-      ar = fma(fu1.x, fw1.x, ar);
-      ar = fma(-fu1.y, fw1.y, ar);
-      ai = fma(fu1.x, fw1.y, ai);
-      ai = fma(fu1.y, fw1.x, ai);
-      Ts[(P.rc_lo + tid / NT) * TS + tid % NT] = make_double2(ar, ai);
     }
   }
   cp_async_wait<0>();
