@@ -373,26 +373,10 @@ __host__ __device__ constexpr size_t qfft_smem_bytes(int n, int NT) {
          (size_t)n * 4 + 64;
 }
 
-template <int N, int NT, int NTHR, int MINB>
-__global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
-  constexpr int L = (N - 1) / 2;
-  // epilogue: (NTHR / NT) * NT threads own (column, row-set) pairs; the rest only reduce
-  static_assert(NTHR >= NT, "threads must cover the columns");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* Ts = reinterpret_cast<double2*>(smem_raw);
-  constexpr int TS = qfft_row_stride(N, NT);  // tile row stride
-  double2* rou_s = Ts + N * TS;
-  double* betaw_s = reinterpret_cast<double*>(rou_s + N);
-  int* perm_s = reinterpret_cast<int*>(betaw_s + (L + 1));
-  const int tid = threadIdx.x;
-  for (int i = tid; i < N; i += NTHR) {
-    rou_s[i] = P.rou[i];
-    perm_s[i] = P.perm[i];
-  }
-  for (int i = tid; i <= L; i += NTHR) betaw_s[i] = P.betaw[i];
-  const int ct = blockIdx.x, comp = blockIdx.y;
-  const int col0 = ct * NT;
-  {
+// The tile load of the alpha pass, shared by k_qfft and k_qfft_half: asynchronous copies of the
+// stored T rows of (comp, 32 columns) into Ts, and the rows k_tgemm left out recomputed from U, W.
+template <int N, int NT, int NTHR, int TS>
+__device__ __forceinline__ void qfft_load_tile(const QfParams& P, double2* Ts, int comp, int col0, int tid) {
     // The rows k_tgemm left out (at most KC terms each, summed in increasing p). With KC = 2 or 4
     // every thread owns KC / 2 (row, column) items (rows g and g + 4 of a thread group g pair a
     // long row with a short one): their operands are requested right after the tile's copies,
@@ -466,7 +450,28 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
         }
       }
     }
+}
+
+template <int N, int NT, int NTHR, int MINB>
+__global__ void __launch_bounds__(NTHR, MINB) k_qfft(const QfParams P) {
+  constexpr int L = (N - 1) / 2;
+  // epilogue: (NTHR / NT) * NT threads own (column, row-set) pairs; the rest only reduce
+  static_assert(NTHR >= NT, "threads must cover the columns");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Ts = reinterpret_cast<double2*>(smem_raw);
+  constexpr int TS = qfft_row_stride(N, NT);  // tile row stride
+  double2* rou_s = Ts + N * TS;
+  double* betaw_s = reinterpret_cast<double*>(rou_s + N);
+  int* perm_s = reinterpret_cast<int*>(betaw_s + (L + 1));
+  const int tid = threadIdx.x;
+  for (int i = tid; i < N; i += NTHR) {
+    rou_s[i] = P.rou[i];
+    perm_s[i] = P.perm[i];
   }
+  for (int i = tid; i <= L; i += NTHR) betaw_s[i] = P.betaw[i];
+  const int ct = blockIdx.x, comp = blockIdx.y;
+  const int col0 = ct * NT;
+  qfft_load_tile<N, NT, NTHR, TS>(P, Ts, comp, col0, tid);
   cp_async_wait<0>();
   __syncthreads();
 
@@ -631,6 +636,103 @@ __global__ void __launch_bounds__(NTHR, MINB) k_qfft_lean(const QfParams P) {
     }
   }
   __syncthreads();
+  const CompRec rec = P.comps[comp];
+  const bool mir = P.mirror && rec.m > 0;
+  const long long sbit = (long long)0x8000000000000000ULL;
+  const long long mflip_r = (rec.m & 1) ? sbit : 0, mflip_i = (rec.m & 1) ? 0 : sbit;
+  double s2 = 0.0, pr = 0.0, pi = 0.0, ir = 0.0, ii = 0.0, g0r = 0.0, g0i = 0.0;
+  long long mx2 = 0;
+  for (int item = tid; item < NT * R1; item += NTHR) {
+    const int c = item % NT, bl = item / NT;
+    const int col = col0 + c;
+    if (col >= P.ncol) continue;
+    double xr[R2], xi[R2];
+    const double2* base = Ts + (size_t)(bl * R2) * NT + c;
+#pragma unroll
+    for (int jj = 0; jj < R2; ++jj) {
+      const double2 v = base[jj * NT];
+      xr[jj] = v.x;
+      xi[jj] = v.y;
+    }
+    double2* o = P.out + rec.slot * P.vol + col;
+    double2* om = mir ? P.out + rec.mslot * P.vol + col : nullptr;
+    const double qb = betaw_s[col / N];
+    double sr = 0.0, si = 0.0;
+    auto emit = [&](int jj, double vr, double vi) {
+      const int a = bl + R1 * jj;  // output frequency of position bl R2 + jj
+      const size_t idx = (size_t)a * P.rpitch;
+      __stcs(o + idx, make_double2(vr, vi));
+      if (om) {
+        const long long br = __double_as_longlong(vr) ^ mflip_r;
+        const long long bi = __double_as_longlong(vi) ^ mflip_i;
+        __stcs(om + idx, make_double2(__longlong_as_double(br), __longlong_as_double(bi)));
+      }
+      const double a2 = fma(vr, vr, vi * vi);
+      s2 += a2;
+      mx2 = max(mx2, __double_as_longlong(a2));
+      const double wgt = digest_weight((uint32_t)((size_t)a * P.ncol + col) * 0x9E3779B1u);
+      pr = fma(wgt, vr, pr);
+      pi = fma(wgt, vi, pi);
+      sr += vr;
+      si += vi;
+      if (a == 0 && col == 0) {
+        g0r = vr;
+        g0i = vi;
+      }
+    };
+    if constexpr (R2 >= kSinkMinRadix) {
+      Radix<R2>::dft_sink(xr, xi, emit);
+    } else {
+      Radix<R2>::dft(xr, xi);
+#pragma unroll
+      for (int jj = 0; jj < R2; ++jj) emit(jj, xr[jj], xi[jj]);
+    }
+    ir = fma(qb, sr, ir);
+    ii = fma(qb, si, ii);
+  }
+  double v[8] = {s2, __longlong_as_double(mx2), pr, pi, g0r, g0i, ir, ii};
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double x = __shfl_down_sync(0xffffffffu, v[q], off);
+      v[q] = (q == 1) ? fmax(v[q], x) : v[q] + x;
+    }
+  if (lane == 0) {
+    double* part = P.partials + (((size_t)comp * P.n_tiles + ct) * (NTHR / 32) + warp) * 8;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) part[q] = v[q];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_qfft_half: k_qfft with its last DIF stage fused into the epilogue (N = R1 R2: 49, 65). The
+// tile load (cp.async, recomputed rows) and the first stage (radix R1, in shared memory) are
+// k_qfft's; the last stage reads its R2 rows into registers and its outputs go straight to the
+// volume rows, the mirror and the digest (as in k_qfft_lean): four shared-memory passes per
+// sample instead of six, no permutation lookups, two barriers fewer; one digest partial per
+// warp. Volumes bitwise equal to k_qfft's, digests associated differently.
+template <int N, int NT, int NTHR, int MINB>
+__global__ void __launch_bounds__(NTHR, MINB) k_qfft_half(const QfParams P) {
+  constexpr int L = (N - 1) / 2;
+  constexpr int R1 = smallest_prime_factor(N), R2 = N / R1;
+  static_assert(R1 * R2 == N && smallest_prime_factor(R2) == R2, "N must be a product of two primes");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Ts = reinterpret_cast<double2*>(smem_raw);
+  constexpr int TS = NT;
+  double2* rou_s = Ts + N * TS;
+  double* betaw_s = reinterpret_cast<double*>(rou_s + N);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < N; i += NTHR) rou_s[i] = P.rou[i];
+  for (int i = tid; i <= L; i += NTHR) betaw_s[i] = P.betaw[i];
+  const int ct = blockIdx.x, comp = blockIdx.y;
+  const int col0 = ct * NT;
+  qfft_load_tile<N, NT, NTHR, TS>(P, Ts, comp, col0, tid);
+  cp_async_wait<0>();
+  __syncthreads();
+  fft_stage_ct<N, R1, N, NT, NT, NTHR, false>(Ts, rou_s, tid);
+  __syncthreads();
+
   const CompRec rec = P.comps[comp];
   const bool mir = P.mirror && rec.m > 0;
   const long long sbit = (long long)0x8000000000000000ULL;

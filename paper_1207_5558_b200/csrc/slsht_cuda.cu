@@ -159,6 +159,7 @@ struct slsht_cuda_plan {
   int tp_KPsub = 0;        //   rows of k_tgemm's range (whole stages)
   short tp_rc_urow[16] = {};
   signed char tp_rc_k[16] = {};
+  bool tp_half = false;    //   k_qfft_half (n = 49, 65): last DIF stage fused into the epilogue, 4 partials per tile
   bool tp_lean = false;    //   k_qfft_lean (n = 49, 65): two smem passes, 4 digest partials per tile
   int tp_pipe_fv = 0;      //   lean alpha pass with per-warp digest partials (4 per tile)
   int* d_tp_sync = nullptr;
@@ -531,6 +532,14 @@ void build_plan(slsht_cuda_plan* p) {
   {
     const char* e = std::getenv("SLSHT_CUDA_TWO_PASS");
     p->use_tp = !(e && e[0] == '0') && tp_kernel(p->n, p->tp_fft, p->tp_threads, p->tp_nt);
+    if (const char* hf = std::getenv("SLSHT_CUDA_QFFT_HALF")) {
+      const int mb = std::atoi(hf);  // CTAs per SM (0: off)
+      if (p->use_tp && mb > 0 && (p->n == 49 || p->n == 65)) {
+        p->tp_half = true;
+        if (p->n == 49) p->tp_fft = mb >= 8 ? k_qfft_half<49, 32, 128, 8> : mb >= 6 ? k_qfft_half<49, 32, 128, 6> : k_qfft_half<49, 32, 128, 5>;
+        else p->tp_fft = mb >= 6 ? k_qfft_half<65, 32, 128, 6> : mb >= 5 ? k_qfft_half<65, 32, 128, 5> : k_qfft_half<65, 32, 128, 4>;
+      }
+    }
     if (const char* ln = std::getenv("SLSHT_CUDA_QFFT_LEAN")) {
       const int mb = std::atoi(ln);  // CTAs per SM of the lean alpha pass (0: off)
       if (p->use_tp && mb > 0 && (p->n == 49 || p->n == 65)) {
@@ -1072,7 +1081,7 @@ void build_plan(slsht_cuda_plan* p) {
                  "device output buffer does not fit in HBM (use the streaming ring mode)"};
   p->d_out = palloc<double2>(p, (size_t)p->n_slots * p->vstride);
   if (p->use_tp) p->d_T = palloc<double2>(p, t_bytes / 16);
-  const int parts_per_tile = p->use_fused ? FuCfg<49>::EPW : ((p->tp_pipe && p->tp_pipe_fv) || p->tp_lean) ? TP_THREADS / 32 : 1;
+  const int parts_per_tile = p->use_fused ? FuCfg<49>::EPW : ((p->tp_pipe && p->tp_pipe_fv) || p->tp_lean || p->tp_half) ? TP_THREADS / 32 : 1;
   p->d_partials = palloc<double>(p, (size_t)p->max_chunk * p->n_col_tiles * parts_per_tile * 8);
   p->digest_rows = coeff_count(p->lmax);
   p->d_digest = palloc<double>(p, (size_t)p->digest_rows * 8);
@@ -1495,7 +1504,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
     p->tp_fft<<<dim3(p->tp_ntiles, ch.count), p->tp_threads, p->tp_fft_smem, fs>>>(qf);
     CKL();
     if (overlap) {
-      k_digest<<<(ch.count + 3) / 4, 128, 0, fs>>>(comps, ch.count, p->n_col_tiles * (p->tp_lean ? TP_THREADS / 32 : 1), p->n,
+      k_digest<<<(ch.count + 3) / 4, 128, 0, fs>>>(comps, ch.count, p->n_col_tiles * ((p->tp_lean || p->tp_half) ? TP_THREADS / 32 : 1), p->n,
                                                     p->d_partials, p->mirror, p->d_digest);
       CKL();
       CK(cudaEventRecord(p->ev_fft[b], fs));
@@ -1515,7 +1524,7 @@ void run_chunk(slsht_cuda_plan* p, const Chunk& ch) {
   k_digest<<<(ch.count + 3) / 4, 128, 0, s>>>(comps, ch.count,
                                                   p->use_lines   ? p->lines_nseg_dig
                                                   : p->use_fused ? p->n_col_tiles * FuCfg<49>::EPW
-                                                  : ((p->tp_pipe && p->tp_pipe_fv) || p->tp_lean) ? p->n_col_tiles * (TP_THREADS / 32)
+                                                  : ((p->tp_pipe && p->tp_pipe_fv) || p->tp_lean || p->tp_half) ? p->n_col_tiles * (TP_THREADS / 32)
                                                                  : p->n_col_tiles,
                                                   p->n, p->d_partials, p->mirror, p->d_digest);
   CKL();

@@ -30,6 +30,8 @@ CASES = [  # (L_f, L_h, real_mode, lmax, engine knobs)
     (2, 32, True, 9, {"SLSHT_CUDA_TP_PIPE": "1", "SLSHT_CUDA_TP_FV": "1"}),    # k_tpipe<65, 1>
     (3, 24, True, 6, {"SLSHT_CUDA_QFFT_LEAN": "6"}),                           # k_qfft_lean<49>
     (2, 32, False, 5, {"SLSHT_CUDA_QFFT_LEAN": "4"}),                          # k_qfft_lean<65>
+    (3, 24, True, 6, {"SLSHT_CUDA_QFFT_HALF": "6"}),                           # k_qfft_half<49>
+    (2, 32, False, 5, {"SLSHT_CUDA_QFFT_HALF": "5"}),                          # k_qfft_half<65>
 ]
 
 
