@@ -37,7 +37,7 @@ struct TgParams {
   int count, KP, ncolp, n;
   int ustride;           // row stride of U (complex); KP may cover a sub-range of the rows
   int col_fast;          // 1: blockIdx.x = column tile (W L2-resident, U block read once)
-  int t_stream;          // 1: T stored with the evict-first (.cs) hint; 2: timing experiment, no T stores
+  int t_stream;          // 1: T stored with the evict-first (.cs) hint; 2 (builds with -DSLSHT_TG_NOSTORE): no T stores
 };
 
 __host__ __device__ constexpr int tgemm_threads(int BN, int WNF, int BM = TG_BM) {
@@ -167,7 +167,11 @@ __global__ void __launch_bounds__(tgemm_threads(BN, WNF, BM), MINB) k_tgemm(cons
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
           const int comp = scomp + mi * 8;
+#ifdef SLSHT_TG_NOSTORE  // timing builds only: the sweep without the q-end sums, addresses and stores
           if (comp < P.count && P.t_stream != 2) {
+#else
+          if (comp < P.count) {
+#endif
             double2* dst = tbase + (size_t)mi * tstep + row * P.ncolp;
 #pragma unroll
             for (int ni = 0; ni < WNF; ++ni) {  // 32 B per lane: 4 lanes write one whole 128-B line
